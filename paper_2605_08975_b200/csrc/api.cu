@@ -1,0 +1,502 @@
+// extern "C" boundary (include/alpa_action.h).  Maps the reference's
+// exception taxonomy onto return codes and owns the K-loop CUDA graph.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+
+#include "ctx.h"
+
+using alpa::Ctx;
+using alpa::Error;
+using alpa::fail;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+template <typename Fn>
+int guarded(Ctx* c, Fn&& fn) {
+    try {
+        fn();
+        return ALPA_OK;
+    } catch (const Error& e) {
+        g_last_error = e.what();
+        if (c) c->err = e.what();
+        return e.code;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        if (c) c->err = e.what();
+        return ALPA_ERR_INTERNAL;
+    }
+}
+
+// ModelConfig::validate (model.cpp:9-24) plus this build's kernel limits.
+void validate(const alpa_model_cfg& c) {
+    if (c.decoder_blocks < 1) fail(ALPA_ERR_CONFIG, "decoder_blocks must be >= 1");
+    if (c.vision_blocks < 0) fail(ALPA_ERR_CONFIG, "vision_blocks must be >= 0");
+    if (c.hidden_dim < 1 || c.action_hidden_dim < 1)
+        fail(ALPA_ERR_CONFIG, "hidden dimensions must be positive");
+    if (c.heads < 1 || c.kv_dim < 1 || c.kv_dim % c.heads != 0)
+        fail(ALPA_ERR_CONFIG, "kv_dim must be a positive multiple of heads");
+    if (c.vocab_size < 128) fail(ALPA_ERR_CONFIG, "vocab_size must be >= 128");
+    if (c.patch_size < 1) fail(ALPA_ERR_CONFIG, "patch_size must be >= 1");
+    if (c.action_steps != 64) fail(ALPA_ERR_CONFIG, "action_steps must be 64");
+    if (c.diffusion_iters < 1) fail(ALPA_ERR_CONFIG, "diffusion_iters must be >= 1");
+    if (!(c.update_scale > 0.0f)) fail(ALPA_ERR_CONFIG, "update_scale must be > 0");
+    if (c.kv_dim / c.heads > 128) fail(ALPA_ERR_CONFIG, "head_dim must be <= 128 in this build");
+    if (c.dtype != ALPA_DTYPE_F32 && c.dtype != ALPA_DTYPE_BF16)
+        fail(ALPA_ERR_CONFIG, "dtype must be ALPA_DTYPE_F32 or ALPA_DTYPE_BF16");
+    if (c.dtype == ALPA_DTYPE_BF16 && (c.action_hidden_dim % 128 != 0 || c.kv_dim % 128 != 0))
+        fail(ALPA_ERR_CONFIG,
+             "bf16 tensor-core path needs action_hidden_dim and kv_dim multiples of 128");
+}
+
+// Rng::normal (common.cpp:48-55) over splitmix64 (common.hpp:36-59): host
+// side so the noise is bit-identical to the reference's (glibc logf/sqrtf/cosf).
+struct HostRng {
+    uint64_t s;
+    uint64_t next() {
+        uint64_t z = (s += 0x9e3779b97f4a7c15ULL);
+        z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+        z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+        return z ^ (z >> 31);
+    }
+    float next_float() { return static_cast<float>(next() >> 40) * (1.0f / 16777216.0f); }
+    float normal() {
+        float u1 = next_float();
+        float u2 = next_float();
+        if (u1 < 1e-12f) u1 = 1e-12f;
+        const float r = std::sqrt(-2.0f * std::log(u1));
+        return r * std::cos(6.28318530717958647692f * u2);
+    }
+};
+
+void* pinned(Ctx& c, size_t elems) {
+    if (c.pinned_elems < elems) {
+        if (c.pinned) cudaFreeHost(c.pinned);
+        c.pinned = nullptr;
+        ALPA_CUDA(cudaMallocHost(&c.pinned, elems * sizeof(float)));
+        c.pinned_elems = elems;
+    }
+    return c.pinned;
+}
+
+void check_request(Ctx& c, const alpa_request& r) {
+    if (!c.weights_ready) fail(ALPA_ERR_INTERNAL, "weights not loaded");
+    if (r.num_trajectories < 1) fail(ALPA_ERR_CONFIG, "num_trajectories must be >= 1");
+    if (r.executor == ALPA_EXEC_GRAPH && r.kv_strategy == ALPA_KV_DYNAMIC)
+        fail(ALPA_ERR_CONFIG,
+             "graph executor requires the static kv strategy (fixed buffer addresses)");
+    if (!c.prefix) fail(ALPA_ERR_INTERNAL, "kv cache: action KV write before reasoning sealed");
+    if (r.topology == ALPA_TOPOLOGY_SINGLE) {
+        if (c.prefix_n != 1)
+            fail(ALPA_ERR_INTERNAL, "replicate_for_batch: source cache must have batch 1");
+    } else {
+        // Multi topology: the cache batch must equal N (pipeline.cpp:411-413)
+        // unless an explicit lane map was bound.
+        if (c.lane_map_host.empty() && c.prefix_n != r.num_trajectories && c.prefix_n != 1)
+            fail(ALPA_ERR_INTERNAL, "kv batch does not match the requested trajectory count");
+    }
+    if (!(r.v0 >= 0.0f) || !std::isfinite(r.v0))
+        fail(ALPA_ERR_INTERNAL, "actions_to_trajectory: invalid initial speed");
+}
+
+void upload_lane_map(Ctx& c, const alpa_request& r) {
+    const int64_t n = r.num_trajectories;
+    std::vector<int32_t> map(n, 0);
+    if (r.topology != ALPA_TOPOLOGY_SINGLE) {
+        if (!c.lane_map_host.empty()) {
+            for (int64_t l = 0; l < n; ++l)
+                map[l] = c.lane_map_host[(size_t)std::min<int64_t>(l, (int64_t)c.lane_map_host.size() - 1)];
+        } else if (c.prefix_n == n) {
+            for (int64_t l = 0; l < n; ++l) map[l] = (int32_t)l;
+        }
+    }
+    for (int32_t v : map)
+        if (v < 0 || v >= c.prefix_n) fail(ALPA_ERR_CONFIG, "lane prefix index out of range");
+    ALPA_CUDA(cudaMemcpyAsync(c.ws.lane_map, map.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice,
+                              c.stream));
+}
+
+// Runs the whole K loop + rollout on c.ws buffers (actions already there).
+// Graph executor: the K iterations and the rollout are ONE captured CUDA
+// graph (model.cpp:607-636 captures one iteration and replays it K-2 times;
+// here the whole loop replays with no host round-trip).  v0 and the
+// non-finite flag live in device scalars so the graph is reusable.
+void run_loop(Ctx& c, const alpa_request& r, int64_t K, alpa_stats* st) {
+    const int64_t n = r.num_trajectories;
+    cudaStream_t s = c.stream;
+    const float v0 = r.v0;
+    ALPA_CUDA(cudaMemcpyAsync(c.d_scalars, &v0, sizeof(float), cudaMemcpyHostToDevice, s));
+    if (r.executor == ALPA_EXEC_GRAPH) {
+        if (!c.graph.exec || c.graph.n != n || c.graph.k != K) {
+            alpa::invalidate_graph(c);
+            cudaGraph_t g = nullptr;
+            ALPA_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+            c.last_launches = 0;
+            try {
+                for (int64_t it = 0; it < K; ++it) alpa::enqueue_iteration(c, n, s);
+                alpa::enqueue_rollout(c, n, c.ws.actions, c.ws.traj, s);
+            } catch (...) {
+                cudaStreamEndCapture(s, &g);
+                if (g) cudaGraphDestroy(g);
+                throw;
+            }
+            ALPA_CUDA(cudaStreamEndCapture(s, &g));
+            ALPA_CUDA(cudaGraphInstantiate(&c.graph.exec, g, 0));
+            cudaGraphDestroy(g);
+            c.graph.n = n;
+            c.graph.k = K;
+            c.graph.nodes = c.last_launches;
+        }
+        ALPA_CUDA(cudaGraphLaunch(c.graph.exec, s));
+        if (st) {
+            st->graph_launches = 1;
+            st->graph_nodes = c.graph.nodes;
+            st->kernel_launches = c.graph.nodes;
+        }
+    } else {
+        c.last_launches = 0;
+        for (int64_t it = 0; it < K; ++it) alpa::enqueue_iteration(c, n, s);
+        alpa::enqueue_rollout(c, n, c.ws.actions, c.ws.traj, s);
+        if (st) {
+            st->graph_launches = 0;
+            st->graph_nodes = 0;
+            st->kernel_launches = c.last_launches;
+        }
+    }
+}
+
+int64_t kv_bytes(const Ctx& c, const alpa_request& r) {
+    // footprint_bytes (kv_cache.cpp:365-372): live tokens r + 64 per lane of
+    // the (replicated) cache, f32 elements, every block.
+    return c.cfg.decoder_blocks * r.num_trajectories * (c.prefix_r + c.steps()) * c.kv() * 2 * 4;
+}
+
+}  // namespace
+
+void alpa::Ctx::dfree(void* p) {
+    for (size_t i = 0; i < allocations.size(); ++i)
+        if (allocations[i] == p) {
+            cudaFree(p);
+            allocations.erase(allocations.begin() + i);
+            return;
+        }
+}
+
+extern "C" {
+
+const char* alpa_version(void) { return "alpa_action 0.1 sm_100a"; }
+
+void alpa_default_cfg(alpa_model_cfg* c) {
+    // fixtures/default_config.json model block
+    std::memset(c, 0, sizeof(*c));
+    c->vision_blocks = 4;
+    c->decoder_blocks = 6;
+    c->hidden_dim = 64;
+    c->action_hidden_dim = 32;
+    c->kv_dim = 32;
+    c->heads = 4;
+    c->vocab_size = 512;
+    c->patch_size = 14;
+    c->action_steps = 64;
+    c->diffusion_iters = 10;
+    c->update_scale = 0.1f;
+    c->dtype = ALPA_DTYPE_F32;
+    c->weight_seed = 1234;
+}
+
+int alpa_validate_cfg(const alpa_model_cfg* cfg) {
+    return guarded(nullptr, [&] {
+        if (!cfg) fail(ALPA_ERR_CONFIG, "null config");
+        validate(*cfg);
+    });
+}
+
+int alpa_ctx_create(const alpa_model_cfg* cfg, int device, alpa_ctx** out) {
+    Ctx* c = nullptr;
+    int rc = guarded(nullptr, [&] {
+        if (!cfg || !out) fail(ALPA_ERR_CONFIG, "null argument");
+        validate(*cfg);
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev < 1)
+            fail(ALPA_ERR_INTERNAL, "no CUDA device available (this library has no CPU fallback)");
+        if (device < 0 || device >= ndev) fail(ALPA_ERR_CONFIG, "device index out of range");
+        ALPA_CUDA(cudaSetDevice(device));
+        cudaDeviceProp prop{};
+        ALPA_CUDA(cudaGetDeviceProperties(&prop, device));
+        if (prop.major != 10)
+            fail(ALPA_ERR_INTERNAL, std::string("sm_100a build needs a Blackwell B200, got ") + prop.name);
+        c = new Ctx();
+        c->cfg = *cfg;
+        c->device = device;
+        ALPA_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        c->own_stream = true;
+        ALPA_CUDA(cudaEventCreate(&c->ev0));
+        ALPA_CUDA(cudaEventCreate(&c->ev1));
+        c->d_scalars = (float*)c->dalloc(16 * sizeof(float));
+        ALPA_CUDA(cudaMemset(c->d_scalars, 0, 16 * sizeof(float)));
+    });
+    if (rc != ALPA_OK) {
+        delete c;
+        return rc;
+    }
+    *out = reinterpret_cast<alpa_ctx*>(c);
+    return ALPA_OK;
+}
+
+void alpa_ctx_destroy(alpa_ctx* h) {
+    Ctx* c = reinterpret_cast<Ctx*>(h);
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->stream) cudaStreamSynchronize(c->stream);
+    if (c->graph.exec) cudaGraphExecDestroy(c->graph.exec);
+    for (void* p : c->allocations) cudaFree(p);
+    if (c->pinned) cudaFreeHost(c->pinned);
+    if (c->ev0) cudaEventDestroy(c->ev0);
+    if (c->ev1) cudaEventDestroy(c->ev1);
+    if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+}
+
+const char* alpa_last_error(const alpa_ctx* h) {
+    const Ctx* c = reinterpret_cast<const Ctx*>(h);
+    return c ? c->err.c_str() : g_last_error.c_str();
+}
+
+int alpa_set_stream(alpa_ctx* h, void* stream) {
+    Ctx* c = reinterpret_cast<Ctx*>(h);
+    return guarded(c, [&] {
+        if (!c) fail(ALPA_ERR_CONFIG, "null context");
+        cudaSetDevice(c->device);
+        cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+        if (!s) {
+            if (!c->own_stream) {
+                ALPA_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+                c->own_stream = true;
+            }
+            return;
+        }
+        if (c->own_stream && c->stream) {
+            cudaStreamSynchronize(c->stream);
+            cudaStreamDestroy(c->stream);
+        }
+        c->stream = s;
+        c->own_stream = false;
+    });
+}
+
+int64_t alpa_weight_stream_offset(const alpa_model_cfg* cfg) { return alpa::stream_offset(*cfg); }
+int64_t alpa_action_param_count(const alpa_model_cfg* cfg) { return alpa::param_count(*cfg); }
+
+int alpa_load_weights_seeded(alpa_ctx* h, uint64_t seed, int64_t offset) {
+    Ctx* c = reinterpret_cast<Ctx*>(h);
+    return guarded(c, [&] {
+        if (!c) fail(ALPA_ERR_CONFIG, "null context");
+        cudaSetDevice(c->device);
+        if (c->weights_ready) fail(ALPA_ERR_INTERNAL, "weights already loaded on this context");
+        alpa::load_weights(*c, nullptr, 0, seed, offset < 0 ? alpa::stream_offset(c->cfg) : offset);
+    });
+}
+
+int alpa_load_weights_host(alpa_ctx* h, const float* arena, int64_t count) {
+    Ctx* c = reinterpret_cast<Ctx*>(h);
+    return guarded(c, [&] {
+        if (!c || !arena) fail(ALPA_ERR_CONFIG, "null argument");
+        cudaSetDevice(c->device);
+        if (c->weights_ready) fail(ALPA_ERR_INTERNAL, "weights already loaded on this context");
+        alpa::load_weights(*c, arena, count, 0, 0);
+    });
+}
+
+int alpa_bind_prefix(alpa_ctx* h, const float* kv, int64_t n_prefix, int64_t r) {
+    Ctx* c = reinterpret_cast<Ctx*>(h);
+    return guarded(c, [&] {
+        if (!c || !kv) fail(ALPA_ERR_CONFIG, "null argument");
+        cudaSetDevice(c->device);
+        alpa::make_prefix_from_host(*c, kv, n_prefix, r);
+        alpa::invalidate_graph(*c);
+    });
+}
+
+int alpa_bind_prefix_device(alpa_ctx* h, const void* kv, int64_t n_prefix, int64_t r) {
+    Ctx* c = reinterpret_cast<Ctx*>(h);
+    return guarded(c, [&] {
+        if (!c || !kv) fail(ALPA_ERR_CONFIG, "null argument");
+        if (r < 1) fail(ALPA_ERR_INTERNAL, "kv cache: sealing an empty reasoning region");
+        if (n_prefix < 1) fail(ALPA_ERR_CONFIG, "prefix count must be >= 1");
+        if (c->prefix && c->own_prefix) c->dfree(c->prefix);
+        c->prefix = const_cast<void*>(kv);
+        c->own_prefix = false;
+        c->prefix_n = n_prefix;
+        c->prefix_r = r;
+        alpa::invalidate_graph(*c);
+    });
+}
+
+int alpa_bind_prefix_synthetic(alpa_ctx* h, uint64_t seed, int64_t r) {
+    Ctx* c = reinterpret_cast<Ctx*>(h);
+    return guarded(c, [&] {
+        if (!c) fail(ALPA_ERR_CONFIG, "null context");
+        cudaSetDevice(c->device);
+        alpa::make_prefix_synthetic(*c, seed, r);
+        alpa::invalidate_graph(*c);
+    });
+}
+
+int alpa_prefix_device(alpa_ctx* h, void** ptr, int64_t* bytes) {
+    Ctx* c = reinterpret_cast<Ctx*>(h);
+    return guarded(c, [&] {
+        if (!c || !ptr || !bytes) fail(ALPA_ERR_CONFIG, "null argument");
+        if (!c->prefix) fail(ALPA_ERR_INTERNAL, "no prefix bound");
+        *ptr = c->prefix;
+        *bytes = c->prefix_n * c->cfg.decoder_blocks * 2 * c->prefix_r * c->kv() * (int64_t)c->esz();
+    });
+}
+
+int alpa_set_lane_prefix(alpa_ctx* h, const int32_t* map, int64_t n) {
+    Ctx* c = reinterpret_cast<Ctx*>(h);
+    return guarded(c, [&] {
+        if (!c) fail(ALPA_ERR_CONFIG, "null context");
+        c->lane_map_host.assign(map, map + (map ? n : 0));
+    });
+}
+
+int alpa_generate(alpa_ctx* h, const alpa_request* req, float* actions_out, float* traj_out,
+                  alpa_stats* st) {
+    Ctx* c = reinterpret_cast<Ctx*>(h);
+    return guarded(c, [&] {
+        if (!c || !req) fail(ALPA_ERR_CONFIG, "null argument");
+        cudaSetDevice(c->device);
+        const alpa_request& r = *req;
+        check_request(*c, r);
+        const int64_t n = r.num_trajectories, A = c->steps();
+        const int64_t K = r.diffusion_iters > 0 ? r.diffusion_iters : c->cfg.diffusion_iters;
+        alpa::ensure_workspace(*c, n);
+        upload_lane_map(*c, r);
+        const size_t na = n * A * 2, nt = n * A * 3;
+        float* host = static_cast<float*>(pinned(*c, na + nt + 1));
+        // host noise (pipeline.cpp:415-424), lane seeds keep the global index
+        for (int64_t l = 0; l < n; ++l) {
+            HostRng rng{r.action_init_seed + static_cast<uint64_t>(r.lane0 + l) * r.action_seed_stride};
+            for (int64_t i = 0; i < A * 2; ++i) host[l * A * 2 + i] = rng.normal();
+        }
+        ALPA_CUDA(cudaEventRecord(c->ev0, c->stream));
+        ALPA_CUDA(cudaMemcpyAsync(c->ws.actions, host, na * sizeof(float), cudaMemcpyHostToDevice,
+                                  c->stream));
+        if (st) std::memset(st, 0, sizeof(*st));
+        run_loop(*c, r, K, st);
+        float* hact = host;
+        float* htraj = host + na;
+        ALPA_CUDA(cudaMemcpyAsync(hact, c->ws.actions, na * sizeof(float), cudaMemcpyDeviceToHost,
+                                  c->stream));
+        ALPA_CUDA(cudaMemcpyAsync(htraj, c->ws.traj, nt * sizeof(float), cudaMemcpyDeviceToHost,
+                                  c->stream));
+        ALPA_CUDA(cudaMemcpyAsync(htraj + nt, c->d_scalars + 1, sizeof(int),
+                                  cudaMemcpyDeviceToHost, c->stream));
+        ALPA_CUDA(cudaEventRecord(c->ev1, c->stream));
+        ALPA_CUDA(cudaStreamSynchronize(c->stream));
+        ALPA_CUDA(cudaGetLastError());
+        int bad = 0;
+        std::memcpy(&bad, htraj + nt, sizeof(int));
+        if (actions_out) std::memcpy(actions_out, hact, na * sizeof(float));
+        if (bad) fail(ALPA_ERR_INTERNAL, "actions_to_trajectory: non-finite action");
+        if (traj_out) std::memcpy(traj_out, htraj, nt * sizeof(float));
+        if (st) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+            st->device_ms = ms;
+            st->kv_bytes = kv_bytes(*c, r);
+            st->h2d_bytes = (int64_t)(na * sizeof(float));
+            st->d2h_bytes = (int64_t)((na + nt) * sizeof(float));
+        }
+    });
+}
+
+int alpa_generate_device(alpa_ctx* h, const alpa_request* req, const float* d_noise,
+                         float* d_actions, float* d_traj, alpa_stats* st) {
+    Ctx* c = reinterpret_cast<Ctx*>(h);
+    return guarded(c, [&] {
+        if (!c || !req || !d_noise) fail(ALPA_ERR_CONFIG, "null argument");
+        cudaSetDevice(c->device);
+        const alpa_request& r = *req;
+        check_request(*c, r);
+        const int64_t n = r.num_trajectories, A = c->steps();
+        const int64_t K = r.diffusion_iters > 0 ? r.diffusion_iters : c->cfg.diffusion_iters;
+        alpa::ensure_workspace(*c, n);
+        upload_lane_map(*c, r);
+        const size_t na = n * A * 2, nt = n * A * 3;
+        if (st) std::memset(st, 0, sizeof(*st));
+        if (st) ALPA_CUDA(cudaEventRecord(c->ev0, c->stream));
+        ALPA_CUDA(cudaMemcpyAsync(c->ws.actions, d_noise, na * sizeof(float),
+                                  cudaMemcpyDeviceToDevice, c->stream));
+        run_loop(*c, r, K, st);
+        if (d_actions)
+            ALPA_CUDA(cudaMemcpyAsync(d_actions, c->ws.actions, na * sizeof(float),
+                                      cudaMemcpyDeviceToDevice, c->stream));
+        if (d_traj)
+            ALPA_CUDA(cudaMemcpyAsync(d_traj, c->ws.traj, nt * sizeof(float),
+                                      cudaMemcpyDeviceToDevice, c->stream));
+        if (st) {
+            ALPA_CUDA(cudaEventRecord(c->ev1, c->stream));
+            ALPA_CUDA(cudaStreamSynchronize(c->stream));
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, c->ev0, c->ev1);
+            st->device_ms = ms;
+            st->kv_bytes = kv_bytes(*c, r);
+        }
+    });
+}
+
+void alpa_host_noise(uint64_t seed, uint64_t stride, int64_t lane0, int64_t n, int64_t steps,
+                     float* out) {
+    for (int64_t l = 0; l < n; ++l) {
+        HostRng rng{seed + static_cast<uint64_t>(lane0 + l) * stride};
+        for (int64_t i = 0; i < steps * 2; ++i) out[l * steps * 2 + i] = rng.normal();
+    }
+}
+
+float alpa_initial_speed(const float* h) {
+    // initial_speed_from_history (pipeline.cpp:150-156)
+    const double dx = static_cast<double>(h[15 * 3]) - h[14 * 3];
+    const double dy = static_cast<double>(h[15 * 3 + 1]) - h[14 * 3 + 1];
+    return static_cast<float>(std::sqrt(dx * dx + dy * dy) / 0.1);
+}
+
+int alpa_rollout(alpa_ctx* h, const float* actions, int64_t n, float v0, float* traj) {
+    Ctx* c = reinterpret_cast<Ctx*>(h);
+    return guarded(c, [&] {
+        if (!c || !actions || !traj) fail(ALPA_ERR_CONFIG, "null argument");
+        if (!(v0 >= 0.0f) || !std::isfinite(v0))
+            fail(ALPA_ERR_INTERNAL, "actions_to_trajectory: invalid initial speed");
+        if (n < 1) return;
+        cudaSetDevice(c->device);
+        const int64_t A = c->steps();
+        float *da = nullptr, *dt = nullptr;
+        ALPA_CUDA(cudaMalloc(&da, n * A * 2 * sizeof(float)));
+        ALPA_CUDA(cudaMalloc(&dt, n * A * 3 * sizeof(float)));
+        ALPA_CUDA(cudaMemcpyAsync(da, actions, n * A * 2 * sizeof(float), cudaMemcpyHostToDevice,
+                                  c->stream));
+        ALPA_CUDA(cudaMemcpyAsync(c->d_scalars, &v0, sizeof(float), cudaMemcpyHostToDevice,
+                                  c->stream));
+        alpa::enqueue_rollout(*c, n, da, dt, c->stream);
+        int hbad = 0;
+        ALPA_CUDA(cudaMemcpyAsync(traj, dt, n * A * 3 * sizeof(float), cudaMemcpyDeviceToHost,
+                                  c->stream));
+        ALPA_CUDA(cudaMemcpyAsync(&hbad, c->d_scalars + 1, sizeof(int), cudaMemcpyDeviceToHost,
+                                  c->stream));
+        ALPA_CUDA(cudaStreamSynchronize(c->stream));
+        cudaFree(da);
+        cudaFree(dt);
+        if (hbad) fail(ALPA_ERR_INTERNAL, "actions_to_trajectory: non-finite action");
+    });
+}
+
+int64_t alpa_kv_footprint_bytes(int64_t blocks, int64_t batch, int64_t tokens, int64_t kv_dim,
+                                int64_t elem_bytes) {
+    // kv_cache.cpp:22-26
+    return blocks * batch * tokens * kv_dim * 2 * elem_bytes;
+}
+
+}  // extern "C"

@@ -1,0 +1,127 @@
+// Internal context of the action-generation library (not part of the ABI).
+#pragma once
+
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/alpa_action.h"
+
+namespace alpa {
+
+// Error carrying one of the ALPA_ERR_* codes (reference taxonomy,
+// common.hpp:10-23).
+struct Error : std::runtime_error {
+    int code;
+    Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void fail(int code, const std::string& m) { throw Error(code, m); }
+
+#define ALPA_CUDA(call)                                                                    \
+    do {                                                                                   \
+        cudaError_t e_ = (call);                                                           \
+        if (e_ != cudaSuccess)                                                             \
+            ::alpa::fail(ALPA_ERR_INTERNAL, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+    } while (0)
+
+// One linear layer on device.  f32 path: w [in][out] (reference layout,
+// model.hpp:57).  bf16 path: w = W^T [out][in] bf16 (K-major tcgen05 operand).
+struct Linear {
+    void* w = nullptr;
+    float* b = nullptr;
+    int64_t in = 0, out = 0;
+    CUtensorMap tmap{};  // bf16: TMA map of W^T, box {64, 128}
+};
+
+struct Block {
+    Linear qkv;  // fused [ah -> 3kv]: q | k | v columns (model.cpp:574-576)
+    Linear o, mlp1, mlp2;
+};
+
+struct Workspace {
+    int64_t n = 0;  // lanes the buffers are sized for
+    float* actions = nullptr;  // [N][64][2]
+    float* traj = nullptr;     // [N][64][3]
+    float* e = nullptr;        // residual stream f32 [M][ah]
+    void* x = nullptr;         // LN output / encoder input: f32 or bf16 [M][ah]
+    void* qkv = nullptr;       // [M][3kv]: q | action K | action V (in place, no copy)
+    void* ctxb = nullptr;      // attention output [M][kv]
+    void* h1 = nullptr;        // MLP hidden [M][4ah]
+    float* splitk = nullptr;   // deterministic split-K partials
+    size_t splitk_elems = 0;
+    int* counters = nullptr;   // split-K tile arrival counters
+    int32_t* lane_map = nullptr;  // [N] prefix index per lane
+    CUtensorMap tm_x{}, tm_ctx{}, tm_h1{};  // bf16 activation maps (B operand)
+    int tn = 64;                            // token tile
+};
+
+struct GraphCache {
+    cudaGraphExec_t exec = nullptr;
+    int64_t n = -1, k = -1;
+    int64_t nodes = 0;
+};
+
+struct Ctx {
+    alpa_model_cfg cfg{};
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    std::string err;
+
+    bool weights_ready = false;
+    Linear act_in, mlp1, mlp2, head;  // act_in/head always f32 [in][out]
+    std::vector<Block> blocks;
+    float* pos = nullptr;  // [64][ah] sinusoid (model.cpp:56-68)
+    std::vector<void*> allocations;
+
+    void* prefix = nullptr;  // [n_prefix][B][2][r][kv] f32 or bf16
+    bool own_prefix = false;
+    int64_t prefix_n = 0, prefix_r = 0;
+    std::vector<int32_t> lane_map_host;  // multi topology
+
+    Workspace ws;
+    GraphCache graph;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    float* d_scalars = nullptr;  // [0] = v0 (rollout), [1] = non-finite flag (int)
+    float* pinned = nullptr;  // host staging
+    size_t pinned_elems = 0;
+    int64_t last_launches = 0;  // kernels enqueued by the last iteration body
+
+    bool bf16() const { return cfg.dtype == ALPA_DTYPE_BF16; }
+    int64_t ah() const { return cfg.action_hidden_dim; }
+    int64_t kv() const { return cfg.kv_dim; }
+    int64_t steps() const { return cfg.action_steps; }
+    size_t esz() const { return bf16() ? 2 : 4; }
+
+    void* dalloc(size_t bytes) {
+        void* p = nullptr;
+        ALPA_CUDA(cudaMalloc(&p, bytes < 16 ? 16 : bytes));
+        allocations.push_back(p);
+        return p;
+    }
+    void dfree(void* p);
+};
+
+// weights.cu
+void load_weights(Ctx& c, const float* host_arena, int64_t count, uint64_t seed, int64_t offset);
+void make_prefix_synthetic(Ctx& c, uint64_t seed, int64_t r);
+void make_prefix_from_host(Ctx& c, const float* host, int64_t n_prefix, int64_t r);
+int64_t stream_offset(const alpa_model_cfg& c);
+int64_t param_count(const alpa_model_cfg& c);
+
+// path.cu
+void ensure_workspace(Ctx& c, int64_t n);
+void enqueue_iteration(Ctx& c, int64_t n, cudaStream_t s);  // one diffusion iteration
+void enqueue_rollout(Ctx& c, int64_t n, const float* d_actions, float* d_traj, cudaStream_t s);
+void invalidate_graph(Ctx& c);
+
+// tma.cu
+void make_tmap_bf16_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
+                       uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer);
+
+}  // namespace alpa

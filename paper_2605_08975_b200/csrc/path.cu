@@ -1,0 +1,563 @@
+// The denoising iteration (Model::run_action_iteration, model.cpp:600-605) as
+// a fixed kernel sequence, plus the device rollout.
+//
+// Per iteration (M = 64 N action rows of all trajectories):
+//   encode      e0 = a.W_in + b_in + pos                      (model.cpp:558-559)
+//   gemm        h1 = gelu(e0.W1 + b1)                         (model.cpp:560-561)
+//   gemm        e  = h1.W2 + b2                               (model.cpp:562)
+//   per block:  x = LN1(e); qkv = x.Wqkv + b (K/V land in the per-lane action
+//               region, no write_action_kv copy); ctx = attn(q, [prefix_b || own
+//               action K/V]); e += ctx.Wo + bo; x = LN2(e); h1 = gelu(x.W1+b1);
+//               e += h1.W2 + b2                               (model.cpp:571-589)
+//   head        a += s * (LN_f(e).Wh + bh)                    (model.cpp:590-598)
+// f32 path: SIMT FFMA kernels.  bf16 path: tcgen05 GEMMs (tc_gemm.cuh), fp32
+// residual stream, fp32 LN/softmax statistics.
+#include <algorithm>
+#include <cstdio>
+
+#include "common.cuh"
+#include "ctx.h"
+#include "tc_gemm.cuh"
+
+namespace alpa {
+
+namespace {
+
+bool pdl_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char* e = getenv("ALPA_PDL");
+        v = (e && e[0] == '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+
+template <typename... KArgs, typename... Args>
+void launch(Ctx& c, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+            Args... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    ALPA_CUDA(cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...));
+    c.last_launches++;
+}
+
+// ------------------------------------------------------------------ encode
+// e0[t][j] = ((a0*w0j + a1*w1j) + b_j) + pos[t%64][j] with the reference's
+// rounding sequence (matmul acc from 0, then bias add, then position add).
+template <typename T>
+__global__ void encode_kernel(const float* __restrict__ act, const float* __restrict__ w,
+                              const float* __restrict__ b, const float* __restrict__ pos,
+                              T* __restrict__ out, int64_t M, int64_t ah, int64_t A) {
+    pdl_wait();
+    pdl_launch();
+    const int64_t total = M * ah;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t t = i / ah, j = i % ah;
+        float acc = __fmul_rn(act[t * 2], w[j]);
+        acc = __fadd_rn(acc, __fmul_rn(act[t * 2 + 1], w[ah + j]));
+        acc = __fadd_rn(acc, b[j]);
+        acc = __fadd_rn(acc, pos[(t % A) * ah + j]);
+        if constexpr (sizeof(T) == 2)
+            out[i] = __float2bfloat16_rn(acc);
+        else
+            out[i] = acc;
+    }
+}
+
+// ------------------------------------------------------------------ layernorm
+// layernorm_row (kernels_serial.cpp:66-84), gamma=1 beta=0, eps=1e-5:
+// mean, two-pass variance, inv = 1/sqrt(var+eps).  One warp per row.
+template <typename T>
+__global__ void layernorm_kernel(const float* __restrict__ x, T* __restrict__ out, int64_t M,
+                                 int64_t n) {
+    pdl_wait();
+    pdl_launch();
+    const int64_t row = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (row >= M) return;
+    const float* xr = x + row * n;
+    float s = 0.f;
+    for (int64_t j = lane; j < n; j += 32) s += xr[j];
+    const float mean = warp_sum(s) / (float)n;
+    float v = 0.f;
+    for (int64_t j = lane; j < n; j += 32) {
+        const float d = xr[j] - mean;
+        v += d * d;
+    }
+    const float var = warp_sum(v) / (float)n;
+    const float inv = 1.0f / sqrtf(var + 1e-5f);
+    T* o = out + row * n;
+    for (int64_t j = lane; j < n; j += 32) {
+        const float y = (xr[j] - mean) * inv;
+        if constexpr (sizeof(T) == 2)
+            o[j] = __float2bfloat16_rn(y);
+        else
+            o[j] = y;
+    }
+}
+
+// ------------------------------------------------------------------ f32 GEMM
+// out[t][n] (op)= sum_k A[t][k] W[k][n] + b[n]; W in the reference [in][out]
+// layout.  64x64 tile, 16-deep k slab, 4x4 register micro-tile (FFMA).
+template <int EPI>
+__global__ void __launch_bounds__(256)
+    gemm_f32_kernel(const float* __restrict__ A, int64_t lda, const float* __restrict__ W,
+                    int64_t ldw, const float* __restrict__ bias, float* out, int64_t ldo, int T,
+                    int N, int K) {
+    pdl_wait();
+    pdl_launch();
+    __shared__ float As[16][64 + 4];
+    __shared__ float Ws[16][64];
+    const int tid = threadIdx.x, ty = tid / 16, tx = tid % 16;
+    const int m0 = blockIdx.y * 64, n0 = blockIdx.x * 64;
+    float acc[4][4] = {};
+    for (int k0 = 0; k0 < K; k0 += 16) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int e = tid + u * 256;  // 0..1023
+            const int r = e / 16, cc = e % 16;
+            const int gm = m0 + r, gk = k0 + cc;
+            As[cc][r] = (gm < T && gk < K) ? A[(int64_t)gm * lda + gk] : 0.f;
+            const int wr = e / 64, wc = e % 64;
+            const int wk = k0 + wr, wn = n0 + wc;
+            Ws[wr][wc] = (wk < K && wn < N) ? W[(int64_t)wk * ldw + wn] : 0.f;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) {
+            float av[4], bv[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) av[i] = As[kk][ty * 4 + i];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) bv[j] = Ws[kk][tx * 4 + j];
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+#pragma unroll
+                for (int j = 0; j < 4; ++j) acc[i][j] += av[i] * bv[j];
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        const int t = m0 + ty * 4 + i;
+        if (t >= T) continue;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const int n = n0 + tx * 4 + j;
+            if (n >= N) continue;
+            const float v = acc[i][j] + bias[n];
+            float* o = out + (int64_t)t * ldo + n;
+            if constexpr (EPI == EPI_GELU_BF16)
+                *o = gelu_erf(v);
+            else if constexpr (EPI == EPI_RESID_F32)
+                *o = *o + v;
+            else
+                *o = v;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ attention
+// emit_attention (model.cpp:280-324) over attend_view (kv_cache.cpp:247-263):
+// lane l, head h, action query i attends [prefix(l) rows 0..r-1 || lane l's 64
+// action rows]; scores alpha*dot (alpha after the dot, kernels_serial.cpp:24),
+// non-causal softmax, P.V.  Warp per query row, online softmax over 32-key
+// chunks (warp-level max/sum), each lane owns head dims lane+32u.
+// The prefix is read in place for every lane: no replicate_for_batch copy.
+template <typename T>
+__global__ void __launch_bounds__(256)
+    attn_simt_kernel(const T* __restrict__ qkv, const T* __restrict__ prefix,
+                     int64_t prefix_stride, int64_t block_off, const int32_t* __restrict__ lane_map,
+                     int n, int r, int kv, int H, int A, float alpha, T* __restrict__ ctx) {
+    pdl_wait();
+    pdl_launch();
+    __shared__ float qs[8][128];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t gw = blockIdx.x * 8 + warp;  // (l, h, i)
+    const int hd = kv / H;
+    if (gw >= (int64_t)n * H * A) return;
+    const int i = gw % A, h = (gw / A) % H, l = gw / ((int64_t)A * H);
+    const int64_t ld = 3 * (int64_t)kv;
+    const T* qrow = qkv + ((int64_t)l * A + i) * ld + h * hd;
+    for (int d = lane; d < hd; d += 32) qs[warp][d] = to_f(qrow[d]);
+    __syncwarp();
+    const T* pk = prefix + lane_map[l] * prefix_stride + block_off + h * hd;
+    const T* pv = pk + (int64_t)r * kv;
+    const T* ak = qkv + (int64_t)l * A * ld + kv + h * hd;
+    const T* av = ak + kv;
+    const int Ttot = r + A;
+    float m = -INFINITY, lsum = 0.f;
+    float o[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int j0 = 0; j0 < Ttot; j0 += 32) {
+        const int j = j0 + lane;
+        float s = -INFINITY;
+        if (j < Ttot) {
+            const T* krow = j < r ? pk + (int64_t)j * kv : ak + (int64_t)(j - r) * ld;
+            float acc = 0.f;
+            for (int d = 0; d < hd; ++d) acc += qs[warp][d] * to_f(krow[d]);
+            s = alpha * acc;
+        }
+        const float mn = fmaxf(m, warp_max(s));
+        const float scale = __expf(m - mn);
+        const float p = (j < Ttot) ? expf(s - mn) : 0.f;
+        lsum = lsum * scale + warp_sum(p);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) o[u] *= scale;
+        const int jn = min(32, Ttot - j0);
+        for (int jj = 0; jj < jn; ++jj) {
+            const float pj = __shfl_sync(0xffffffffu, p, jj);
+            const int jt = j0 + jj;
+            const T* vrow = jt < r ? pv + (int64_t)jt * kv : av + (int64_t)(jt - r) * ld;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int d = lane + 32 * u;
+                if (d < hd) o[u] += pj * to_f(vrow[d]);
+            }
+        }
+        m = mn;
+    }
+    const float inv = 1.0f / lsum;
+    T* orow = ctx + ((int64_t)l * A + i) * kv + h * hd;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int d = lane + 32 * u;
+        if (d < hd) {
+            if constexpr (sizeof(T) == 2)
+                orow[d] = __float2bfloat16_rn(o[u] * inv);
+            else
+                orow[d] = o[u] * inv;
+        }
+    }
+}
+
+// ------------------------------------------------------------------ head + update
+// delta = LN_f(e).Wh + bh (model.cpp:590-591); a = a + (s*delta)
+// (model.cpp:594-598, two separate roundings).  One warp per action row.
+__global__ void head_update_kernel(const float* __restrict__ e, const float* __restrict__ wh,
+                                   const float* __restrict__ bh, float* __restrict__ act,
+                                   int64_t M, int64_t ah, float scale) {
+    pdl_wait();
+    pdl_launch();
+    const int64_t row = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (row >= M) return;
+    const float* xr = e + row * ah;
+    float s = 0.f;
+    for (int64_t j = lane; j < ah; j += 32) s += xr[j];
+    const float mean = warp_sum(s) / (float)ah;
+    float v = 0.f;
+    for (int64_t j = lane; j < ah; j += 32) {
+        const float d = xr[j] - mean;
+        v += d * d;
+    }
+    const float inv = 1.0f / sqrtf(warp_sum(v) / (float)ah + 1e-5f);
+    float d0 = 0.f, d1 = 0.f;
+    for (int64_t j = lane; j < ah; j += 32) {
+        const float y = (xr[j] - mean) * inv;
+        d0 += y * wh[j * 2];
+        d1 += y * wh[j * 2 + 1];
+    }
+    d0 = warp_sum(d0);
+    d1 = warp_sum(d1);
+    if (lane == 0) {
+        const float delta0 = d0 + bh[0], delta1 = d1 + bh[1];
+        act[row * 2] = __fadd_rn(act[row * 2], __fmul_rn(scale, delta0));
+        act[row * 2 + 1] = __fadd_rn(act[row * 2 + 1], __fmul_rn(scale, delta1));
+    }
+}
+
+// ------------------------------------------------------------------ rollout
+// actions_to_trajectory (pipeline.cpp:124-148): fp64 explicit Euler unicycle,
+// dt = 0.1, every update from the old state, pose = float cast.  sin/cos are
+// evaluated in double-double and rounded once, so they match a correctly
+// rounded libm (glibc) bit for bit; no FMA contraction anywhere.
+struct dd {
+    double hi, lo;
+};
+__device__ inline dd two_sum(double a, double b) {
+    const double s = __dadd_rn(a, b);
+    const double bb = __dsub_rn(s, a);
+    const double err = __dadd_rn(__dsub_rn(a, __dsub_rn(s, bb)), __dsub_rn(b, bb));
+    return {s, err};
+}
+__device__ inline dd quick_two_sum(double a, double b) {
+    const double s = __dadd_rn(a, b);
+    return {s, __dsub_rn(b, __dsub_rn(s, a))};
+}
+__device__ inline dd dd_add(dd a, dd b) {
+    dd s = two_sum(a.hi, b.hi);
+    const dd t = two_sum(a.lo, b.lo);
+    s.lo = __dadd_rn(s.lo, t.hi);
+    s = quick_two_sum(s.hi, s.lo);
+    s.lo = __dadd_rn(s.lo, t.lo);
+    return quick_two_sum(s.hi, s.lo);
+}
+__device__ inline dd dd_mul(dd a, dd b) {
+    const double p = __dmul_rn(a.hi, b.hi);
+    double e = __fma_rn(a.hi, b.hi, -p);
+    e = __dadd_rn(e, __dadd_rn(__dmul_rn(a.hi, b.lo), __dmul_rn(a.lo, b.hi)));
+    return quick_two_sum(p, e);
+}
+__device__ inline dd dd_mul_d(dd a, double b) {
+    const double p = __dmul_rn(a.hi, b);
+    double e = __fma_rn(a.hi, b, -p);
+    e = __dadd_rn(e, __dmul_rn(a.lo, b));
+    return quick_two_sum(p, e);
+}
+__device__ inline dd dd_div_d(dd a, double b) {
+    const double q1 = __ddiv_rn(a.hi, b);
+    const dd p = {__dmul_rn(q1, b), __fma_rn(q1, b, -__dmul_rn(q1, b))};
+    const double r = __dadd_rn(__dsub_rn(__dsub_rn(a.hi, p.hi), p.lo), a.lo);
+    return quick_two_sum(q1, __ddiv_rn(r, b));
+}
+
+__device__ void sincos_dd(double x, double* sn, double* cs) {
+    // Cody-Waite reduction by pi/2 with a 3-part constant (fdlibm split).
+    const double k = rint(__dmul_rn(x, 6.36619772367581382433e-01));
+    const double p1 = 1.57079632673412561417e+00, p2 = 6.07710050630396597660e-11,
+                 p3 = 2.02226624871116645580e-21, p3t = 8.47842766036889956997e-32;
+    dd r = two_sum(x, -__dmul_rn(k, p1));  // k*p1 exact for |k| < 2^20
+    r = dd_add(r, dd{-__dmul_rn(k, p2), -__fma_rn(k, p2, -__dmul_rn(k, p2))});
+    r = dd_add(r, dd{-__dmul_rn(k, p3), -__fma_rn(k, p3, -__dmul_rn(k, p3))});
+    r = dd_add(r, dd{-__dmul_rn(k, p3t), 0.0});
+    const dd r2 = dd_mul(r, r);
+    // Taylor series to degree 27 / 26 (|r| <= pi/4: truncation < 1e-31 rel).
+    dd term = r, s = r;
+    for (int n = 3; n <= 27; n += 2) {
+        term = dd_div_d(dd_mul(term, r2), -(double)((n - 1) * n));
+        s = dd_add(s, term);
+    }
+    dd tc = {1.0, 0.0}, c = {1.0, 0.0};
+    for (int n = 2; n <= 26; n += 2) {
+        tc = dd_div_d(dd_mul(tc, r2), -(double)((n - 1) * n));
+        c = dd_add(c, tc);
+    }
+    const double sh = __dadd_rn(s.hi, s.lo), ch = __dadd_rn(c.hi, c.lo);
+    const long q = ((long)k) & 3;
+    if (q == 0) { *sn = sh; *cs = ch; }
+    else if (q == 1) { *sn = ch; *cs = -sh; }
+    else if (q == 2) { *sn = -sh; *cs = -ch; }
+    else { *sn = -ch; *cs = sh; }
+}
+
+__global__ void rollout_kernel(const float* __restrict__ act, float* __restrict__ traj, int n,
+                               int steps, const float* __restrict__ v0p, int* __restrict__ bad) {
+    pdl_wait();
+    pdl_launch();
+    const int l = blockIdx.x * blockDim.x + threadIdx.x;
+    if (l >= n) return;
+    double x = 0.0, y = 0.0, yaw = 0.0, v = (double)(*v0p);
+    const double dt = 0.1;
+    for (int i = 0; i < steps; ++i) {
+        const float a = act[((int64_t)l * steps + i) * 2];
+        const float k = act[((int64_t)l * steps + i) * 2 + 1];
+        if (!isfinite(a) || !isfinite(k)) atomicExch(bad, 1);
+        double sy, cy;
+        sincos_dd(yaw, &sy, &cy);
+        const double nx = __dadd_rn(x, __dmul_rn(__dmul_rn(v, cy), dt));
+        const double ny = __dadd_rn(y, __dmul_rn(__dmul_rn(v, sy), dt));
+        const double nyaw = __dadd_rn(yaw, __dmul_rn(__dmul_rn((double)k, v), dt));
+        const double nv = __dadd_rn(v, __dmul_rn((double)a, dt));
+        x = nx; y = ny; yaw = nyaw; v = nv;
+        float* p = traj + ((int64_t)l * steps + i) * 3;
+        p[0] = __double2float_rn(x);
+        p[1] = __double2float_rn(y);
+        p[2] = __double2float_rn(yaw);
+    }
+}
+
+inline int ew_grid(int64_t n) {
+    int64_t g = (n + 255) / 256;
+    return (int)std::max<int64_t>(1, std::min<int64_t>(g, 148 * 16));
+}
+
+// ------------------------------------------------------------------ GEMM dispatch
+struct TcPlan {
+    int splits, kbs;
+};
+
+TcPlan plan_tc(int nf, int T, int K, int tn) {
+    const int tiles = (nf / 128) * ((T + tn - 1) / tn);
+    const int KB = K / 64;
+    int splits = std::max(1, std::min(148 / std::max(1, tiles), KB / 4));
+    if (splits < 1) splits = 1;
+    int kbs = (KB + splits - 1) / splits;
+    splits = (KB + kbs - 1) / kbs;  // every split non-empty
+    return {splits, kbs};
+}
+
+template <int TN, int EPI>
+void launch_tc(Ctx& c, const Linear& L, const CUtensorMap& tmx, int T, void* out, int64_t ldo,
+               cudaStream_t s) {
+    using Cf = GemmCfg<TN>;
+    static bool configured = false;
+    if (!configured) {
+        ALPA_CUDA(cudaFuncSetAttribute(tc_gemm_kernel<TN, EPI>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
+        configured = true;
+    }
+    GemmArgs a{};
+    a.nf = (int)L.out;
+    a.t = T;
+    a.k = (int)L.in;
+    a.bias = L.b;
+    a.out = out;
+    a.ldo = ldo;
+    const TcPlan p = plan_tc(a.nf, T, a.k, TN);
+    a.splits = p.splits;
+    a.kbs = p.kbs;
+    a.ws = c.ws.splitk;
+    a.counters = c.ws.counters;
+    if (p.splits > 1 && (size_t)p.splits * T * a.nf > c.ws.splitk_elems)
+        fail(ALPA_ERR_INTERNAL, "split-K workspace too small");
+    dim3 grid(a.nf / 128, (T + TN - 1) / TN, p.splits);
+    launch(c, tc_gemm_kernel<TN, EPI>, grid, dim3(192), (size_t)Cf::SMEM, s, L.tmap, tmx, a);
+}
+
+template <int EPI>
+void gemm_tc(Ctx& c, const Linear& L, const CUtensorMap& tmx, int T, void* out, int64_t ldo,
+             cudaStream_t s) {
+    switch (c.ws.tn) {
+        case 64: launch_tc<64, EPI>(c, L, tmx, T, out, ldo, s); break;
+        case 128: launch_tc<128, EPI>(c, L, tmx, T, out, ldo, s); break;
+        case 192: launch_tc<192, EPI>(c, L, tmx, T, out, ldo, s); break;
+        default: launch_tc<256, EPI>(c, L, tmx, T, out, ldo, s); break;
+    }
+}
+
+template <int EPI>
+void gemm_f32(Ctx& c, const Linear& L, const float* A, int64_t lda, int T, float* out,
+              int64_t ldo, cudaStream_t s) {
+    dim3 grid((unsigned)((L.out + 63) / 64), (unsigned)((T + 63) / 64));
+    launch(c, gemm_f32_kernel<EPI>, grid, dim3(256), 0, s, A, lda, (const float*)L.w, L.out,
+           (const float*)L.b, out, ldo, T, (int)L.out, (int)L.in);
+}
+
+size_t splitk_need(const Ctx& c, int T) {
+    if (!c.bf16()) return 0;
+    size_t need = 0;
+    auto chk = [&](int64_t nf, int64_t K) {
+        const TcPlan p = plan_tc((int)nf, T, (int)K, c.ws.tn);
+        if (p.splits > 1) need = std::max(need, (size_t)p.splits * T * nf);
+    };
+    const int64_t ah = c.ah(), kv = c.kv();
+    chk(4 * ah, ah);
+    chk(ah, 4 * ah);
+    chk(3 * kv, ah);
+    chk(ah, kv);
+    return need;
+}
+
+}  // namespace
+
+void ensure_workspace(Ctx& c, int64_t n) {
+    if (c.ws.n == n) return;
+    // buffers change -> any captured graph is stale
+    invalidate_graph(c);
+    Workspace& w = c.ws;
+    for (void* p : {(void*)w.actions, (void*)w.traj, (void*)w.e, w.x, w.qkv, w.ctxb, w.h1,
+                    (void*)w.splitk, (void*)w.counters, (void*)w.lane_map})
+        if (p) c.dfree(p);
+    w = Workspace{};
+    const int64_t A = c.steps(), M = n * A, ah = c.ah(), kv = c.kv();
+    const size_t es = c.esz();
+    w.n = n;
+    w.actions = (float*)c.dalloc(M * 2 * sizeof(float));
+    w.traj = (float*)c.dalloc(M * 3 * sizeof(float));
+    w.e = (float*)c.dalloc(M * ah * sizeof(float));
+    w.x = c.dalloc(M * ah * es);
+    w.qkv = c.dalloc(M * 3 * kv * es);
+    w.ctxb = c.dalloc(M * kv * es);
+    w.h1 = c.dalloc(M * 4 * ah * es);
+    w.counters = (int*)c.dalloc(8192 * sizeof(int));
+    ALPA_CUDA(cudaMemset(w.counters, 0, 8192 * sizeof(int)));
+    w.lane_map = (int32_t*)c.dalloc(n * sizeof(int32_t));
+    const int T = (int)M;
+    w.tn = (T % 256 == 0) ? 256 : (T % 192 == 0) ? 192 : (T % 128 == 0) ? 128 : 64;
+    if (c.bf16()) {
+        w.splitk_elems = splitk_need(c, T);
+        if (w.splitk_elems) w.splitk = (float*)c.dalloc(w.splitk_elems * sizeof(float));
+        make_tmap_bf16_2d(&w.tm_x, w.x, ah, M, ah * 2, 64, w.tn);
+        make_tmap_bf16_2d(&w.tm_ctx, w.ctxb, kv, M, kv * 2, 64, w.tn);
+        make_tmap_bf16_2d(&w.tm_h1, w.h1, 4 * ah, M, 4 * ah * 2, 64, w.tn);
+    }
+}
+
+void enqueue_iteration(Ctx& c, int64_t n, cudaStream_t s) {
+    Workspace& w = c.ws;
+    const int64_t A = c.steps(), M = n * A, ah = c.ah(), kv = c.kv(), H = c.cfg.heads;
+    const int T = (int)M;
+    const int64_t r = c.prefix_r;
+    const int64_t prefix_stride = c.cfg.decoder_blocks * 2 * r * kv;
+    const float alpha = 1.0f / sqrtf((float)(kv / H));
+    const int ln_grid = (int)((M + 7) / 8);
+    const int attn_grid = (int)((n * H * A + 7) / 8);
+    if (c.bf16()) {
+        using bf = __nv_bfloat16;
+        launch(c, encode_kernel<bf>, dim3(ew_grid(M * ah)), dim3(256), 0, s, w.actions,
+               (const float*)c.act_in.w, c.act_in.b, c.pos, (bf*)w.x, M, ah, A);
+        gemm_tc<EPI_GELU_BF16>(c, c.mlp1, w.tm_x, T, w.h1, 4 * ah, s);
+        gemm_tc<EPI_F32>(c, c.mlp2, w.tm_h1, T, w.e, ah, s);
+        for (int64_t b = 0; b < c.cfg.decoder_blocks; ++b) {
+            const Block& blk = c.blocks[b];
+            launch(c, layernorm_kernel<bf>, dim3(ln_grid), dim3(256), 0, s, (const float*)w.e,
+                   (bf*)w.x, M, ah);
+            gemm_tc<EPI_BF16>(c, blk.qkv, w.tm_x, T, w.qkv, 3 * kv, s);
+            launch(c, attn_simt_kernel<bf>, dim3(attn_grid), dim3(256), 0, s, (const bf*)w.qkv,
+                   (const bf*)c.prefix, prefix_stride, b * 2 * r * kv, (const int32_t*)w.lane_map,
+                   (int)n, (int)r, (int)kv, (int)H, (int)A, alpha, (bf*)w.ctxb);
+            gemm_tc<EPI_RESID_F32>(c, blk.o, w.tm_ctx, T, w.e, ah, s);
+            launch(c, layernorm_kernel<bf>, dim3(ln_grid), dim3(256), 0, s, (const float*)w.e,
+                   (bf*)w.x, M, ah);
+            gemm_tc<EPI_GELU_BF16>(c, blk.mlp1, w.tm_x, T, w.h1, 4 * ah, s);
+            gemm_tc<EPI_RESID_F32>(c, blk.mlp2, w.tm_h1, T, w.e, ah, s);
+        }
+    } else {
+        float* x = (float*)w.x;
+        float* h1 = (float*)w.h1;
+        launch(c, encode_kernel<float>, dim3(ew_grid(M * ah)), dim3(256), 0, s, w.actions,
+               (const float*)c.act_in.w, c.act_in.b, c.pos, x, M, ah, A);
+        gemm_f32<EPI_GELU_BF16>(c, c.mlp1, x, ah, T, h1, 4 * ah, s);
+        gemm_f32<EPI_F32>(c, c.mlp2, h1, 4 * ah, T, w.e, ah, s);
+        for (int64_t b = 0; b < c.cfg.decoder_blocks; ++b) {
+            const Block& blk = c.blocks[b];
+            launch(c, layernorm_kernel<float>, dim3(ln_grid), dim3(256), 0, s, (const float*)w.e, x,
+                   M, ah);
+            gemm_f32<EPI_F32>(c, blk.qkv, x, ah, T, (float*)w.qkv, 3 * kv, s);
+            launch(c, attn_simt_kernel<float>, dim3(attn_grid), dim3(256), 0, s,
+                   (const float*)w.qkv, (const float*)c.prefix, prefix_stride, b * 2 * r * kv,
+                   (const int32_t*)w.lane_map, (int)n, (int)r, (int)kv, (int)H, (int)A, alpha,
+                   (float*)w.ctxb);
+            gemm_f32<EPI_RESID_F32>(c, blk.o, (const float*)w.ctxb, kv, T, w.e, ah, s);
+            launch(c, layernorm_kernel<float>, dim3(ln_grid), dim3(256), 0, s, (const float*)w.e, x,
+                   M, ah);
+            gemm_f32<EPI_GELU_BF16>(c, blk.mlp1, x, ah, T, h1, 4 * ah, s);
+            gemm_f32<EPI_RESID_F32>(c, blk.mlp2, h1, 4 * ah, T, w.e, ah, s);
+        }
+    }
+    launch(c, head_update_kernel, dim3(ln_grid), dim3(256), 0, s, (const float*)w.e,
+           (const float*)c.head.w, (const float*)c.head.b, w.actions, M, ah, c.cfg.update_scale);
+}
+
+void enqueue_rollout(Ctx& c, int64_t n, const float* d_actions, float* d_traj, cudaStream_t s) {
+    int* bad = reinterpret_cast<int*>(c.d_scalars + 1);
+    ALPA_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
+    launch(c, rollout_kernel, dim3((unsigned)((n + 63) / 64)), dim3(64), 0, s, d_actions, d_traj,
+           (int)n, (int)c.steps(), (const float*)c.d_scalars, bad);
+}
+
+void invalidate_graph(Ctx& c) {
+    if (c.graph.exec) cudaGraphExecDestroy(c.graph.exec);
+    c.graph = GraphCache{};
+}
+
+}  // namespace alpa
