@@ -185,7 +185,8 @@ class PortWeights:
         self.cfg = cfg
 
     def arena(self) -> np.ndarray:
-        return np.ctypeslib.as_array(self.w.arena, shape=(self.w.count,))
+        """A copy of the whole arena in draw order (safe after this object dies)."""
+        return np.ctypeslib.as_array(self.w.arena, shape=(self.w.count,)).copy()
 
     def tensor(self, which: str, blk: int | None = None):
         """('w' [in][out], 'b' [out]) numpy views of one linear."""
