@@ -132,6 +132,10 @@ int alpa_bind_prefix_device(alpa_ctx* ctx, const void* kv, int64_t n_prefix, int
 /* make_sealed_cache recipe (tests/test_model.cpp:43-74) generated on device:
  * per block Rng(seed+b) uniform(-0.5,0.5) keys, V = -K. */
 int alpa_bind_prefix_synthetic(alpa_ctx* ctx, uint64_t seed, int64_t r);
+/* Writes the make_sealed_cache recipe for `seed` into a caller device buffer
+ * [B][2][r][kv] in the ctx dtype (scene producer for benches / collectives);
+ * bind it with alpa_bind_prefix_device. */
+int alpa_synthesize_prefix(alpa_ctx* ctx, void* dst, uint64_t seed, int64_t r);
 /* Device pointer/bytes of the bound prefix (for collectives). */
 int alpa_prefix_device(alpa_ctx* ctx, void** ptr, int64_t* bytes);
 /* Multi topology: lane l attends prefix lane_map[l] (default: all 0). */
@@ -147,6 +151,20 @@ int alpa_generate(alpa_ctx* ctx, const alpa_request* req, float* actions_out,
  * HBM (d_actions [N][64][2], d_traj [N][64][3]; d_traj may be NULL). */
 int alpa_generate_device(alpa_ctx* ctx, const alpa_request* req, const float* d_noise,
                          float* d_actions, float* d_traj, alpa_stats* stats);
+
+/* ---- measurement --------------------------------------------------------- */
+/* Per-kernel device time of `iters` eagerly launched iterations (+ rollout),
+ * an event pair around every launch, aggregated by kernel name; flops/bytes
+ * are the algorithmic work of those launches (SURVEY.md §8d accounting). */
+typedef struct alpa_kernel_prof {
+    char name[40];
+    int64_t launches;
+    double total_ms;
+    double flops;
+    double bytes;
+} alpa_kernel_prof;
+int alpa_profile(alpa_ctx* ctx, const alpa_request* req, int64_t iters, alpa_kernel_prof* out,
+                 int32_t max_out, int32_t* n_out);
 
 /* ---- host helpers (bit-exact restatements of the reference host code) -- */
 /* Rng::normal noise for lanes [lane0, lane0+n): out [n][steps][2]. */

@@ -86,6 +86,11 @@ class Stats(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class KernelProf(C.Structure):
+    _fields_ = [("name", C.c_char * 40), ("launches", C.c_int64), ("total_ms", C.c_double),
+                ("flops", C.c_double), ("bytes", C.c_double)]
+
+
 _f32p = C.POINTER(C.c_float)
 _lib = None
 
@@ -116,11 +121,14 @@ def lib():
         L.alpa_bind_prefix.argtypes = [C.c_void_p, _f32p, C.c_int64, C.c_int64]
         L.alpa_bind_prefix_device.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64]
         L.alpa_bind_prefix_synthetic.argtypes = [C.c_void_p, C.c_uint64, C.c_int64]
+        L.alpa_synthesize_prefix.argtypes = [C.c_void_p, C.c_void_p, C.c_uint64, C.c_int64]
         L.alpa_prefix_device.argtypes = [C.c_void_p, P(C.c_void_p), P(C.c_int64)]
         L.alpa_set_lane_prefix.argtypes = [C.c_void_p, P(C.c_int32), C.c_int64]
         L.alpa_generate.argtypes = [C.c_void_p, P(_Req), _f32p, _f32p, P(Stats)]
         L.alpa_generate_device.argtypes = [C.c_void_p, P(_Req), C.c_void_p, C.c_void_p,
                                            C.c_void_p, P(Stats)]
+        L.alpa_profile.argtypes = [C.c_void_p, P(_Req), C.c_int64, P(KernelProf), C.c_int32,
+                                   P(C.c_int32)]
         L.alpa_host_noise.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, C.c_int64, C.c_int64,
                                       _f32p]
         L.alpa_initial_speed.restype = C.c_float
@@ -256,6 +264,15 @@ class ActionGenerator:
     def bind_prefix_device(self, ptr: int, n_prefix: int, r: int) -> None:
         _check(lib().alpa_bind_prefix_device(self._h, C.c_void_p(ptr), n_prefix, r), self._h)
 
+    def synthesize_prefix(self, dst_ptr: int, seed: int, r: int) -> None:
+        """Write the synthetic scene prefix into a caller device buffer (on the
+        ctx stream)."""
+        _check(lib().alpa_synthesize_prefix(self._h, C.c_void_p(dst_ptr), seed, r), self._h)
+
+    def prefix_bytes(self, r: int, n_prefix: int = 1) -> int:
+        es = 2 if DTYPES[self.cfg.dtype] == 1 else 4
+        return n_prefix * self.cfg.decoder_blocks * 2 * r * self.cfg.kv_dim * es
+
     def prefix_device(self) -> tuple[int, int]:
         p, nb = C.c_void_p(), C.c_int64()
         _check(lib().alpa_prefix_device(self._h, C.byref(p), C.byref(nb)), self._h)
@@ -288,6 +305,16 @@ class ActionGenerator:
                                           C.c_void_p(d_actions), C.c_void_p(d_traj or None),
                                           C.byref(st) if st is not None else None), self._h)
         return st.as_dict() if st is not None else None
+
+    def profile(self, req: InferenceRequest, iters: int = 1) -> list[dict]:
+        """Per-kernel CUDA-event times of `iters` eager iterations (+ rollout)."""
+        buf = (KernelProf * 64)()
+        n = C.c_int32()
+        _check(lib().alpa_profile(self._h, C.byref(req._c()), iters, buf, 64, C.byref(n)),
+               self._h)
+        return [dict(name=buf[i].name.decode(), launches=buf[i].launches,
+                     total_ms=buf[i].total_ms, flops=buf[i].flops, bytes=buf[i].bytes)
+                for i in range(n.value)]
 
     def rollout(self, actions: np.ndarray, v0: float) -> np.ndarray:
         a = np.ascontiguousarray(actions, np.float32)

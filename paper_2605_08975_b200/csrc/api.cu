@@ -4,6 +4,8 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <vector>
+#include <algorithm>
 
 #include "ctx.h"
 
@@ -345,6 +347,15 @@ int alpa_bind_prefix_synthetic(alpa_ctx* h, uint64_t seed, int64_t r) {
     });
 }
 
+int alpa_synthesize_prefix(alpa_ctx* h, void* dst, uint64_t seed, int64_t r) {
+    Ctx* c = reinterpret_cast<Ctx*>(h);
+    return guarded(c, [&] {
+        if (!c || !dst) fail(ALPA_ERR_CONFIG, "null argument");
+        cudaSetDevice(c->device);
+        alpa::synthesize_prefix_into(*c, dst, seed, r);
+    });
+}
+
 int alpa_prefix_device(alpa_ctx* h, void** ptr, int64_t* bytes) {
     Ctx* c = reinterpret_cast<Ctx*>(h);
     return guarded(c, [&] {
@@ -446,6 +457,60 @@ int alpa_generate_device(alpa_ctx* h, const alpa_request* req, const float* d_no
             st->device_ms = ms;
             st->kv_bytes = kv_bytes(*c, r);
         }
+    });
+}
+
+int alpa_profile(alpa_ctx* h, const alpa_request* req, int64_t iters, alpa_kernel_prof* out,
+                 int32_t max_out, int32_t* n_out) {
+    Ctx* c = reinterpret_cast<Ctx*>(h);
+    return guarded(c, [&] {
+        if (!c || !req || !out || !n_out) fail(ALPA_ERR_CONFIG, "null argument");
+        cudaSetDevice(c->device);
+        const alpa_request& r = *req;
+        check_request(*c, r);
+        const int64_t n = r.num_trajectories, A = c->steps();
+        alpa::ensure_workspace(*c, n);
+        upload_lane_map(*c, r);
+        std::vector<float> noise(n * A * 2);
+        alpa_host_noise(r.action_init_seed, r.action_seed_stride, r.lane0, n, A, noise.data());
+        ALPA_CUDA(cudaMemcpyAsync(c->ws.actions, noise.data(), noise.size() * sizeof(float),
+                                  cudaMemcpyHostToDevice, c->stream));
+        const float v0 = r.v0;
+        ALPA_CUDA(cudaMemcpyAsync(c->d_scalars, &v0, sizeof(float), cudaMemcpyHostToDevice,
+                                  c->stream));
+        c->prof.clear();
+        c->ev_next = 0;
+        c->prof_on = true;
+        try {
+            for (int64_t it = 0; it < iters; ++it) alpa::enqueue_iteration(*c, n, c->stream);
+            alpa::enqueue_rollout(*c, n, c->ws.actions, c->ws.traj, c->stream);
+        } catch (...) {
+            c->prof_on = false;
+            throw;
+        }
+        c->prof_on = false;
+        ALPA_CUDA(cudaStreamSynchronize(c->stream));
+        std::vector<alpa_kernel_prof> agg;
+        for (const auto& rec : c->prof) {
+            float ms = 0.f;
+            ALPA_CUDA(cudaEventElapsedTime(&ms, rec.a, rec.b));
+            alpa_kernel_prof* slot = nullptr;
+            for (auto& a : agg)
+                if (std::strncmp(a.name, rec.tag, sizeof(a.name)) == 0) slot = &a;
+            if (!slot) {
+                agg.push_back(alpa_kernel_prof{});
+                slot = &agg.back();
+                std::strncpy(slot->name, rec.tag, sizeof(slot->name) - 1);
+            }
+            slot->launches += 1;
+            slot->total_ms += ms;
+            slot->flops += rec.flops;
+            slot->bytes += rec.bytes;
+        }
+        c->prof.clear();
+        const int32_t k = (int32_t)std::min<size_t>(agg.size(), (size_t)max_out);
+        for (int32_t i = 0; i < k; ++i) out[i] = agg[i];
+        *n_out = k;
     });
 }
 

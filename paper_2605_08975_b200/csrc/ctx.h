@@ -52,12 +52,22 @@ struct Workspace {
     void* qkv = nullptr;       // [M][3kv]: q | action K | action V (in place, no copy)
     void* ctxb = nullptr;      // attention output [M][kv]
     void* h1 = nullptr;        // MLP hidden [M][4ah]
-    float* splitk = nullptr;   // deterministic split-K partials
-    size_t splitk_elems = 0;
-    int* counters = nullptr;   // split-K tile arrival counters
+    int* counters = nullptr;   // scratch arrival counters
     int32_t* lane_map = nullptr;  // [N] prefix index per lane
     CUtensorMap tm_x{}, tm_ctx{}, tm_h1{};  // bf16 activation maps (B operand)
     int tn = 64;                            // token tile
+};
+
+// Per-kernel timing records (alpa_profile): an event pair around each launch.
+struct ProfRec {
+    const char* tag;
+    cudaEvent_t a, b;
+    double flops, bytes;
+};
+// Algorithmic work of one launch (SURVEY.md §8d accounting).
+struct KInfo {
+    const char* tag;
+    double flops, bytes;
 };
 
 struct GraphCache {
@@ -91,6 +101,10 @@ struct Ctx {
     float* pinned = nullptr;  // host staging
     size_t pinned_elems = 0;
     int64_t last_launches = 0;  // kernels enqueued by the last iteration body
+    bool prof_on = false;
+    std::vector<ProfRec> prof;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_next = 0;
 
     bool bf16() const { return cfg.dtype == ALPA_DTYPE_BF16; }
     int64_t ah() const { return cfg.action_hidden_dim; }
@@ -110,6 +124,7 @@ struct Ctx {
 // weights.cu
 void load_weights(Ctx& c, const float* host_arena, int64_t count, uint64_t seed, int64_t offset);
 void make_prefix_synthetic(Ctx& c, uint64_t seed, int64_t r);
+void synthesize_prefix_into(Ctx& c, void* dst, uint64_t seed, int64_t r);
 void make_prefix_from_host(Ctx& c, const float* host, int64_t n_prefix, int64_t r);
 int64_t stream_offset(const alpa_model_cfg& c);
 int64_t param_count(const alpa_model_cfg& c);

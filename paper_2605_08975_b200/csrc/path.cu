@@ -32,21 +32,57 @@ bool pdl_enabled() {
     return v == 1;
 }
 
+cudaEvent_t pool_event(Ctx& c) {
+    if (c.ev_next == c.ev_pool.size()) {
+        cudaEvent_t e;
+        ALPA_CUDA(cudaEventCreate(&e));
+        c.ev_pool.push_back(e);
+    }
+    return c.ev_pool[c.ev_next++];
+}
+
 template <typename... KArgs, typename... Args>
-void launch(Ctx& c, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-            Args... args) {
+void launch_cl(Ctx& c, const KInfo& info, dim3 cluster, void (*k)(KArgs...), dim3 grid,
+               dim3 block, size_t smem, cudaStream_t s, Args... args) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = s;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute attr[2];
+    int na = 0;
+    if (pdl_enabled() && !c.prof_on) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    if (cluster.x * cluster.y * cluster.z > 1) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = cluster.x;
+        attr[na].val.clusterDim.y = cluster.y;
+        attr[na].val.clusterDim.z = cluster.z;
+        ++na;
+    }
     cfg.attrs = attr;
-    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    cfg.numAttrs = na;
+    ProfRec rec{info.tag, nullptr, nullptr, info.flops, info.bytes};
+    if (c.prof_on) {
+        rec.a = pool_event(c);
+        rec.b = pool_event(c);
+        ALPA_CUDA(cudaEventRecord(rec.a, s));
+    }
     ALPA_CUDA(cudaLaunchKernelEx(&cfg, k, static_cast<KArgs>(args)...));
+    if (c.prof_on) {
+        ALPA_CUDA(cudaEventRecord(rec.b, s));
+        c.prof.push_back(rec);
+    }
     c.last_launches++;
+}
+
+template <typename... KArgs, typename... Args>
+void launch(Ctx& c, const KInfo& info, void (*k)(KArgs...), dim3 grid, dim3 block, size_t smem,
+            cudaStream_t s, Args... args) {
+    launch_cl(c, info, dim3(1, 1, 1), k, grid, block, smem, s, args...);
 }
 
 // ------------------------------------------------------------------ encode
@@ -385,19 +421,28 @@ struct TcPlan {
     int splits, kbs;
 };
 
+// Split-K count = cluster size: a divisor of the token tile (each split CTA
+// reduces TN/S rows), <= 8 (portable cluster), grid <= one wave of 148 SMs,
+// and at least 2 k-blocks per split.
 TcPlan plan_tc(int nf, int T, int K, int tn) {
     const int tiles = (nf / 128) * ((T + tn - 1) / tn);
     const int KB = K / 64;
-    int splits = std::max(1, std::min(148 / std::max(1, tiles), KB / 4));
-    if (splits < 1) splits = 1;
-    int kbs = (KB + splits - 1) / splits;
-    splits = (KB + kbs - 1) / kbs;  // every split non-empty
-    return {splits, kbs};
+    int best = 1;
+    for (int s : {2, 3, 4, 6, 8})
+        if (tn % s == 0 && tiles * s <= 148 && KB % s == 0 && KB / s >= 2) best = s;
+    return {best, KB / best};
+}
+
+KInfo gemm_info(const char* tag, const Linear& L, int T, size_t esz, int epi) {
+    const double w = (double)L.in * L.out * esz, x = (double)T * L.in * esz;
+    const double o = (double)T * L.out * ((epi == EPI_F32 || epi == EPI_RESID_F32) ? 4 : esz) *
+                     (epi == EPI_RESID_F32 ? 2 : 1);
+    return {tag, 2.0 * T * L.in * L.out, w + x + o};
 }
 
 template <int TN, int EPI>
-void launch_tc(Ctx& c, const Linear& L, const CUtensorMap& tmx, int T, void* out, int64_t ldo,
-               cudaStream_t s) {
+void launch_tc(Ctx& c, const char* tag, const Linear& L, const CUtensorMap& tmx, int T, void* out,
+               int64_t ldo, cudaStream_t s) {
     using Cf = GemmCfg<TN>;
     static bool configured = false;
     if (!configured) {
@@ -415,46 +460,28 @@ void launch_tc(Ctx& c, const Linear& L, const CUtensorMap& tmx, int T, void* out
     const TcPlan p = plan_tc(a.nf, T, a.k, TN);
     a.splits = p.splits;
     a.kbs = p.kbs;
-    a.ws = c.ws.splitk;
-    a.counters = c.ws.counters;
-    if (p.splits > 1 && (size_t)p.splits * T * a.nf > c.ws.splitk_elems)
-        fail(ALPA_ERR_INTERNAL, "split-K workspace too small");
     dim3 grid(a.nf / 128, (T + TN - 1) / TN, p.splits);
-    launch(c, tc_gemm_kernel<TN, EPI>, grid, dim3(192), (size_t)Cf::SMEM, s, L.tmap, tmx, a);
+    launch_cl(c, gemm_info(tag, L, T, 2, EPI), dim3(1, 1, p.splits), tc_gemm_kernel<TN, EPI>, grid,
+              dim3(192), (size_t)Cf::SMEM, s, L.tmap, tmx, a);
 }
 
 template <int EPI>
-void gemm_tc(Ctx& c, const Linear& L, const CUtensorMap& tmx, int T, void* out, int64_t ldo,
-             cudaStream_t s) {
+void gemm_tc(Ctx& c, const char* tag, const Linear& L, const CUtensorMap& tmx, int T, void* out,
+             int64_t ldo, cudaStream_t s) {
     switch (c.ws.tn) {
-        case 64: launch_tc<64, EPI>(c, L, tmx, T, out, ldo, s); break;
-        case 128: launch_tc<128, EPI>(c, L, tmx, T, out, ldo, s); break;
-        case 192: launch_tc<192, EPI>(c, L, tmx, T, out, ldo, s); break;
-        default: launch_tc<256, EPI>(c, L, tmx, T, out, ldo, s); break;
+        case 64: launch_tc<64, EPI>(c, tag, L, tmx, T, out, ldo, s); break;
+        case 128: launch_tc<128, EPI>(c, tag, L, tmx, T, out, ldo, s); break;
+        case 192: launch_tc<192, EPI>(c, tag, L, tmx, T, out, ldo, s); break;
+        default: launch_tc<256, EPI>(c, tag, L, tmx, T, out, ldo, s); break;
     }
 }
 
 template <int EPI>
-void gemm_f32(Ctx& c, const Linear& L, const float* A, int64_t lda, int T, float* out,
-              int64_t ldo, cudaStream_t s) {
+void gemm_f32(Ctx& c, const char* tag, const Linear& L, const float* A, int64_t lda, int T,
+              float* out, int64_t ldo, cudaStream_t s) {
     dim3 grid((unsigned)((L.out + 63) / 64), (unsigned)((T + 63) / 64));
-    launch(c, gemm_f32_kernel<EPI>, grid, dim3(256), 0, s, A, lda, (const float*)L.w, L.out,
-           (const float*)L.b, out, ldo, T, (int)L.out, (int)L.in);
-}
-
-size_t splitk_need(const Ctx& c, int T) {
-    if (!c.bf16()) return 0;
-    size_t need = 0;
-    auto chk = [&](int64_t nf, int64_t K) {
-        const TcPlan p = plan_tc((int)nf, T, (int)K, c.ws.tn);
-        if (p.splits > 1) need = std::max(need, (size_t)p.splits * T * nf);
-    };
-    const int64_t ah = c.ah(), kv = c.kv();
-    chk(4 * ah, ah);
-    chk(ah, 4 * ah);
-    chk(3 * kv, ah);
-    chk(ah, kv);
-    return need;
+    launch(c, gemm_info(tag, L, T, 4, EPI), gemm_f32_kernel<EPI>, grid, dim3(256), 0, s, A, lda,
+           (const float*)L.w, L.out, (const float*)L.b, out, ldo, T, (int)L.out, (int)L.in);
 }
 
 }  // namespace
@@ -465,7 +492,7 @@ void ensure_workspace(Ctx& c, int64_t n) {
     invalidate_graph(c);
     Workspace& w = c.ws;
     for (void* p : {(void*)w.actions, (void*)w.traj, (void*)w.e, w.x, w.qkv, w.ctxb, w.h1,
-                    (void*)w.splitk, (void*)w.counters, (void*)w.lane_map})
+                    (void*)w.counters, (void*)w.lane_map})
         if (p) c.dfree(p);
     w = Workspace{};
     const int64_t A = c.steps(), M = n * A, ah = c.ah(), kv = c.kv();
@@ -484,8 +511,6 @@ void ensure_workspace(Ctx& c, int64_t n) {
     const int T = (int)M;
     w.tn = (T % 256 == 0) ? 256 : (T % 192 == 0) ? 192 : (T % 128 == 0) ? 128 : 64;
     if (c.bf16()) {
-        w.splitk_elems = splitk_need(c, T);
-        if (w.splitk_elems) w.splitk = (float*)c.dalloc(w.splitk_elems * sizeof(float));
         make_tmap_bf16_2d(&w.tm_x, w.x, ah, M, ah * 2, 64, w.tn);
         make_tmap_bf16_2d(&w.tm_ctx, w.ctxb, kv, M, kv * 2, 64, w.tn);
         make_tmap_bf16_2d(&w.tm_h1, w.h1, 4 * ah, M, 4 * ah * 2, 64, w.tn);
@@ -501,57 +526,68 @@ void enqueue_iteration(Ctx& c, int64_t n, cudaStream_t s) {
     const float alpha = 1.0f / sqrtf((float)(kv / H));
     const int ln_grid = (int)((M + 7) / 8);
     const int attn_grid = (int)((n * H * A + 7) / 8);
+    const double es = (double)c.esz();
+    const KInfo enc{"encode", 4.0 * M * ah, M * 2 * 4.0 + M * ah * es};
+    const KInfo ln{"layernorm", 8.0 * M * ah, M * ah * (4.0 + es)};
+    // emit_attention FLOPs: QK^T and PV over r + 64 keys; bytes:
+    // this block's prefix K/V once + q/k/v action rows + ctx.
+    const KInfo att{"attention", 4.0 * n * A * (r + A) * kv,
+                    2.0 * r * kv * es + M * 3.0 * kv * es + M * kv * es};
+    const KInfo head{"head_update", 4.0 * M * ah + 8.0 * M, M * ah * 4.0 + M * 2 * 8.0};
     if (c.bf16()) {
         using bf = __nv_bfloat16;
-        launch(c, encode_kernel<bf>, dim3(ew_grid(M * ah)), dim3(256), 0, s, w.actions,
+        launch(c, enc, encode_kernel<bf>, dim3(ew_grid(M * ah)), dim3(256), 0, s, w.actions,
                (const float*)c.act_in.w, c.act_in.b, c.pos, (bf*)w.x, M, ah, A);
-        gemm_tc<EPI_GELU_BF16>(c, c.mlp1, w.tm_x, T, w.h1, 4 * ah, s);
-        gemm_tc<EPI_F32>(c, c.mlp2, w.tm_h1, T, w.e, ah, s);
+        gemm_tc<EPI_GELU_BF16>(c, "gemm_enc_mlp1", c.mlp1, w.tm_x, T, w.h1, 4 * ah, s);
+        gemm_tc<EPI_F32>(c, "gemm_enc_mlp2", c.mlp2, w.tm_h1, T, w.e, ah, s);
         for (int64_t b = 0; b < c.cfg.decoder_blocks; ++b) {
             const Block& blk = c.blocks[b];
-            launch(c, layernorm_kernel<bf>, dim3(ln_grid), dim3(256), 0, s, (const float*)w.e,
+            launch(c, ln, layernorm_kernel<bf>, dim3(ln_grid), dim3(256), 0, s, (const float*)w.e,
                    (bf*)w.x, M, ah);
-            gemm_tc<EPI_BF16>(c, blk.qkv, w.tm_x, T, w.qkv, 3 * kv, s);
-            launch(c, attn_simt_kernel<bf>, dim3(attn_grid), dim3(256), 0, s, (const bf*)w.qkv,
-                   (const bf*)c.prefix, prefix_stride, b * 2 * r * kv, (const int32_t*)w.lane_map,
-                   (int)n, (int)r, (int)kv, (int)H, (int)A, alpha, (bf*)w.ctxb);
-            gemm_tc<EPI_RESID_F32>(c, blk.o, w.tm_ctx, T, w.e, ah, s);
-            launch(c, layernorm_kernel<bf>, dim3(ln_grid), dim3(256), 0, s, (const float*)w.e,
+            gemm_tc<EPI_BF16>(c, "gemm_qkv", blk.qkv, w.tm_x, T, w.qkv, 3 * kv, s);
+            launch(c, att, attn_simt_kernel<bf>, dim3(attn_grid), dim3(256), 0, s,
+                   (const bf*)w.qkv, (const bf*)c.prefix, prefix_stride, b * 2 * r * kv,
+                   (const int32_t*)w.lane_map, (int)n, (int)r, (int)kv, (int)H, (int)A, alpha,
+                   (bf*)w.ctxb);
+            gemm_tc<EPI_RESID_F32>(c, "gemm_o", blk.o, w.tm_ctx, T, w.e, ah, s);
+            launch(c, ln, layernorm_kernel<bf>, dim3(ln_grid), dim3(256), 0, s, (const float*)w.e,
                    (bf*)w.x, M, ah);
-            gemm_tc<EPI_GELU_BF16>(c, blk.mlp1, w.tm_x, T, w.h1, 4 * ah, s);
-            gemm_tc<EPI_RESID_F32>(c, blk.mlp2, w.tm_h1, T, w.e, ah, s);
+            gemm_tc<EPI_GELU_BF16>(c, "gemm_mlp1", blk.mlp1, w.tm_x, T, w.h1, 4 * ah, s);
+            gemm_tc<EPI_RESID_F32>(c, "gemm_mlp2", blk.mlp2, w.tm_h1, T, w.e, ah, s);
         }
     } else {
         float* x = (float*)w.x;
         float* h1 = (float*)w.h1;
-        launch(c, encode_kernel<float>, dim3(ew_grid(M * ah)), dim3(256), 0, s, w.actions,
+        launch(c, enc, encode_kernel<float>, dim3(ew_grid(M * ah)), dim3(256), 0, s, w.actions,
                (const float*)c.act_in.w, c.act_in.b, c.pos, x, M, ah, A);
-        gemm_f32<EPI_GELU_BF16>(c, c.mlp1, x, ah, T, h1, 4 * ah, s);
-        gemm_f32<EPI_F32>(c, c.mlp2, h1, 4 * ah, T, w.e, ah, s);
+        gemm_f32<EPI_GELU_BF16>(c, "gemm_enc_mlp1", c.mlp1, x, ah, T, h1, 4 * ah, s);
+        gemm_f32<EPI_F32>(c, "gemm_enc_mlp2", c.mlp2, h1, 4 * ah, T, w.e, ah, s);
         for (int64_t b = 0; b < c.cfg.decoder_blocks; ++b) {
             const Block& blk = c.blocks[b];
-            launch(c, layernorm_kernel<float>, dim3(ln_grid), dim3(256), 0, s, (const float*)w.e, x,
-                   M, ah);
-            gemm_f32<EPI_F32>(c, blk.qkv, x, ah, T, (float*)w.qkv, 3 * kv, s);
-            launch(c, attn_simt_kernel<float>, dim3(attn_grid), dim3(256), 0, s,
+            launch(c, ln, layernorm_kernel<float>, dim3(ln_grid), dim3(256), 0, s,
+                   (const float*)w.e, x, M, ah);
+            gemm_f32<EPI_F32>(c, "gemm_qkv", blk.qkv, x, ah, T, (float*)w.qkv, 3 * kv, s);
+            launch(c, att, attn_simt_kernel<float>, dim3(attn_grid), dim3(256), 0, s,
                    (const float*)w.qkv, (const float*)c.prefix, prefix_stride, b * 2 * r * kv,
                    (const int32_t*)w.lane_map, (int)n, (int)r, (int)kv, (int)H, (int)A, alpha,
                    (float*)w.ctxb);
-            gemm_f32<EPI_RESID_F32>(c, blk.o, (const float*)w.ctxb, kv, T, w.e, ah, s);
-            launch(c, layernorm_kernel<float>, dim3(ln_grid), dim3(256), 0, s, (const float*)w.e, x,
-                   M, ah);
-            gemm_f32<EPI_GELU_BF16>(c, blk.mlp1, x, ah, T, h1, 4 * ah, s);
-            gemm_f32<EPI_RESID_F32>(c, blk.mlp2, h1, 4 * ah, T, w.e, ah, s);
+            gemm_f32<EPI_RESID_F32>(c, "gemm_o", blk.o, (const float*)w.ctxb, kv, T, w.e, ah, s);
+            launch(c, ln, layernorm_kernel<float>, dim3(ln_grid), dim3(256), 0, s,
+                   (const float*)w.e, x, M, ah);
+            gemm_f32<EPI_GELU_BF16>(c, "gemm_mlp1", blk.mlp1, x, ah, T, h1, 4 * ah, s);
+            gemm_f32<EPI_RESID_F32>(c, "gemm_mlp2", blk.mlp2, h1, 4 * ah, T, w.e, ah, s);
         }
     }
-    launch(c, head_update_kernel, dim3(ln_grid), dim3(256), 0, s, (const float*)w.e,
+    launch(c, head, head_update_kernel, dim3(ln_grid), dim3(256), 0, s, (const float*)w.e,
            (const float*)c.head.w, (const float*)c.head.b, w.actions, M, ah, c.cfg.update_scale);
 }
 
 void enqueue_rollout(Ctx& c, int64_t n, const float* d_actions, float* d_traj, cudaStream_t s) {
     int* bad = reinterpret_cast<int*>(c.d_scalars + 1);
     ALPA_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), s));
-    launch(c, rollout_kernel, dim3((unsigned)((n + 63) / 64)), dim3(64), 0, s, d_actions, d_traj,
+    const KInfo info{"rollout", 64.0 * n * c.steps(), n * c.steps() * 20.0};
+    launch(c, info, rollout_kernel, dim3((unsigned)((n + 63) / 64)), dim3(64), 0, s, d_actions,
+           d_traj,
            (int)n, (int)c.steps(), (const float*)c.d_scalars, bad);
 }
 

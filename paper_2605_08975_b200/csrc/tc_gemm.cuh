@@ -14,9 +14,15 @@
 // issuer (one elected lane), warps 2..5 = epilogue (TMEM lane quarters
 // 2,3,0,1).  Multi-stage smem ring with full/empty mbarriers.
 //
-// Split-K is deterministic: every split writes its partial tile, the last
-// arriving CTA (tile counter) sums the partials in split order and applies
-// the fused epilogue (bias / GELU / residual), then re-arms the counter.
+// Epilogue: the accumulator is staged TMEM -> registers -> smem (fp32
+// [token][feature], reusing the drained pipeline buffers), then ALL 192
+// threads apply bias / GELU / residual with coalesced 16-byte global
+// accesses along the feature dimension.
+//
+// Split-K is deterministic and on-chip: the S CTAs that share an output tile
+// form one thread-block cluster (1,1,S); after staging, CTA s reduces token
+// rows [s*TN/S, (s+1)*TN/S) by reading all S staged partials through DSMEM in
+// split order, then applies the fused epilogue for those rows.
 #pragma once
 
 #include "common.cuh"
@@ -28,6 +34,7 @@ enum Epi : int {
     EPI_GELU_BF16 = 1,  // out bf16 = gelu(acc + b)                (mlp1 + gelu, model.cpp:585-586)
     EPI_F32 = 2,        // out f32  = acc + b                      (encoder mlp2, model.cpp:562)
     EPI_RESID_F32 = 3,  // out f32  = out + (acc + b)              (o / mlp2 + residual, model.cpp:582-588)
+    EPI_NONE = 4,       // benchmarking only: accumulator discarded
 };
 
 struct GemmArgs {
@@ -35,9 +42,7 @@ struct GemmArgs {
     const float* bias;     // [nf]
     void* out;             // [t][ldo]
     int64_t ldo;
-    int splits, kbs;       // split-K count, 64-wide k-blocks per split
-    float* ws;             // [splits][t][nf] partials (splits > 1)
-    int* counters;         // per output tile
+    int splits, kbs;       // split-K count (= cluster size along z), k-blocks per split
 };
 
 template <int TN>
@@ -50,18 +55,24 @@ struct GemmCfg {
     static constexpr uint32_t TCOLS = TN <= 32 ? 32 : TN <= 64 ? 64 : TN <= 128 ? 128 : 256;
 };
 
+// 4 consecutive features of one token row: v = acc + bias, then the op.
 template <int EPI>
-__device__ inline void epi_store(const GemmArgs& a, int t, int f, float v) {
-    if constexpr (EPI == EPI_BF16) {
-        reinterpret_cast<__nv_bfloat16*>(a.out)[(int64_t)t * a.ldo + f] = __float2bfloat16_rn(v);
-    } else if constexpr (EPI == EPI_GELU_BF16) {
-        reinterpret_cast<__nv_bfloat16*>(a.out)[(int64_t)t * a.ldo + f] =
-            __float2bfloat16_rn(gelu_erf(v));
+__device__ inline void epi_store4(const GemmArgs& a, int t, int f, float4 v) {
+    if constexpr (EPI == EPI_BF16 || EPI == EPI_GELU_BF16) {
+        if constexpr (EPI == EPI_GELU_BF16) {
+            v.x = gelu_erf(v.x); v.y = gelu_erf(v.y); v.z = gelu_erf(v.z); v.w = gelu_erf(v.w);
+        }
+        __nv_bfloat162 lo = __floats2bfloat162_rn(v.x, v.y), hi = __floats2bfloat162_rn(v.z, v.w);
+        uint2 pk;
+        pk.x = *reinterpret_cast<uint32_t*>(&lo);
+        pk.y = *reinterpret_cast<uint32_t*>(&hi);
+        *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(a.out) + (int64_t)t * a.ldo + f) = pk;
     } else if constexpr (EPI == EPI_F32) {
-        reinterpret_cast<float*>(a.out)[(int64_t)t * a.ldo + f] = v;
-    } else {
-        float* o = reinterpret_cast<float*>(a.out) + (int64_t)t * a.ldo + f;
-        *o = *o + v;
+        *reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + (int64_t)t * a.ldo + f) = v;
+    } else if constexpr (EPI == EPI_RESID_F32) {
+        float4* o = reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + (int64_t)t * a.ldo + f);
+        const float4 e = *o;
+        *o = make_float4(e.x + v.x, e.y + v.y, e.z + v.z, e.w + v.w);
     }
 }
 
@@ -77,7 +88,6 @@ __global__ void __launch_bounds__(192, 1)
     uint64_t* empty = full + C::STAGES;
     uint64_t* accf = empty + C::STAGES;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
-    __shared__ int s_last;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int f0 = blockIdx.x * 128, t0 = blockIdx.y * TN;
@@ -143,60 +153,59 @@ __global__ void __launch_bounds__(192, 1)
         }
         __syncwarp();
     } else {
-        // ---------------- epilogue: warps 2..5 ----------------
+        // ---------------- epilogue stage 1: TMEM -> smem (warps 2..5) ---------
         const int q = warp & 3;
-        const int f = f0 + q * 32 + lane;
-        const float bias = a.bias[f];
         const uint32_t trow = tbase + (uint32_t(q * 32) << 16);
+        float* stage = reinterpret_cast<float*>(smem);  // [TN][128] fp32
         mbar_wait(accf, 0);
         tc_fence_after();
-        pdl_launch();
-        if (a.splits == 1) {
-            for (int c = 0; c < TN; c += 16) {
-                uint32_t r[16];
-                tmem_ld16(trow + c, r);
-                tmem_ld_wait();
+        const int fl = q * 32 + lane;
+#pragma unroll 1
+        for (int c = 0; c < TN; c += 16) {
+            uint32_t r[16];
+            tmem_ld16(trow + c, r);
+            tmem_ld_wait();
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const int t = t0 + c + j;
-                    if (t < a.t) epi_store<EPI>(a, t, f, __uint_as_float(r[j]) + bias);
-                }
-            }
-        } else {
-            float* wsz = a.ws + (size_t)blockIdx.z * a.t * a.nf;
-            for (int c = 0; c < TN; c += 16) {
-                uint32_t r[16];
-                tmem_ld16(trow + c, r);
-                tmem_ld_wait();
-#pragma unroll
-                for (int j = 0; j < 16; ++j) {
-                    const int t = t0 + c + j;
-                    if (t < a.t) __stcg(wsz + (size_t)t * a.nf + f, __uint_as_float(r[j]));
-                }
-            }
-            __threadfence();
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            const int tile = blockIdx.y * gridDim.x + blockIdx.x;
-            if (threadIdx.x == 64) {
-                const int old = atomicAdd(&a.counters[tile], 1);
-                s_last = (old == a.splits - 1);
-            }
-            asm volatile("bar.sync 1, 128;" ::: "memory");
-            if (s_last) {
-                __threadfence();
-                const int tend = min(a.t, t0 + TN);
-                for (int t = t0; t < tend; ++t) {
-                    float acc = __ldcg(a.ws + (size_t)t * a.nf + f);
-                    for (int s = 1; s < a.splits; ++s)
-                        acc += __ldcg(a.ws + ((size_t)s * a.t + t) * a.nf + f);
-                    epi_store<EPI>(a, t, f, acc + bias);
-                }
-                if (threadIdx.x == 64) a.counters[tile] = 0;
-            }
+            for (int j = 0; j < 16; ++j) stage[(c + j) * 128 + fl] = __uint_as_float(r[j]);
         }
     }
     tc_fence_before();
     __syncthreads();
+    pdl_launch();
+    // ---------------- epilogue stage 2: reduce + fused op (all 192 threads) -------
+    {
+        const int S = a.splits;
+        const int rows = TN / S;
+        const uint32_t rank = S > 1 ? cluster_ctarank() : 0;
+        if (S > 1) cluster_sync_all();  // every split staged its partial
+        const int r0 = (int)rank * rows;
+        const int fq = (threadIdx.x & 31) * 4;        // 4 features per lane
+        const float4 b4 = *reinterpret_cast<const float4*>(a.bias + f0 + fq);
+        const uint32_t stage_base = smem_u32(smem);
+        uint32_t src[8];
+        for (int s2 = 0; s2 < S; ++s2) src[s2] = S > 1 ? dsmem_addr(stage_base, s2) : stage_base;
+        pdl_wait();  // residual / outputs may be touched by the previous kernel
+#pragma unroll 2
+        for (int rr = threadIdx.x >> 5; rr < rows; rr += 6) {
+            const int tl = r0 + rr;
+            const int t = t0 + tl;
+            const uint32_t off = (uint32_t)(tl * 128 + fq) * 4u;
+            float4 acc;
+            if (S > 1) {
+                acc = ld_dsmem_f4(src[0] + off);
+                for (int s2 = 1; s2 < S; ++s2) {
+                    const float4 p = ld_dsmem_f4(src[s2] + off);
+                    acc.x += p.x; acc.y += p.y; acc.z += p.z; acc.w += p.w;
+                }
+            } else {
+                acc = *reinterpret_cast<const float4*>(smem + off);
+            }
+            if (t < a.t)
+                epi_store4<EPI>(a, t, f0 + fq,
+                                make_float4(acc.x + b4.x, acc.y + b4.y, acc.z + b4.z, acc.w + b4.w));
+        }
+        if (S > 1) cluster_sync_all();  // keep smem alive until every CTA read it
+    }
     if (warp == 1) tmem_dealloc(tbase, C::TCOLS);
 }
 

@@ -210,20 +210,25 @@ static void release_prefix(Ctx& c) {
     c.own_prefix = false;
 }
 
+void synthesize_prefix_into(Ctx& c, void* dst, uint64_t seed, int64_t r) {
+    if (r < 1) fail(ALPA_ERR_INTERNAL, "kv cache: sealing an empty reasoning region");
+    const int64_t B = c.cfg.decoder_blocks, kv = c.cfg.kv_dim;
+    if (c.bf16())
+        synth_prefix<__nv_bfloat16><<<grid_for(B * r * kv), 256, 0, c.stream>>>(
+            seed, B, r, kv, (__nv_bfloat16*)dst);
+    else
+        synth_prefix<float><<<grid_for(B * r * kv), 256, 0, c.stream>>>(seed, B, r, kv,
+                                                                        (float*)dst);
+    ALPA_CUDA(cudaGetLastError());
+}
+
 void make_prefix_synthetic(Ctx& c, uint64_t seed, int64_t r) {
     if (r < 1) fail(ALPA_ERR_INTERNAL, "kv cache: sealing an empty reasoning region");
     release_prefix(c);
-    const int64_t B = c.cfg.decoder_blocks, kv = c.cfg.kv_dim;
-    const int64_t n = B * 2 * r * kv;
+    const int64_t n = c.cfg.decoder_blocks * 2 * r * c.cfg.kv_dim;
     c.prefix = c.dalloc(n * c.esz());
     c.own_prefix = true;
-    if (c.bf16())
-        synth_prefix<__nv_bfloat16><<<grid_for(B * r * kv), 256, 0, c.stream>>>(
-            seed, B, r, kv, (__nv_bfloat16*)c.prefix);
-    else
-        synth_prefix<float><<<grid_for(B * r * kv), 256, 0, c.stream>>>(seed, B, r, kv,
-                                                                        (float*)c.prefix);
-    ALPA_CUDA(cudaGetLastError());
+    synthesize_prefix_into(c, c.prefix, seed, r);
     ALPA_CUDA(cudaStreamSynchronize(c.stream));
     c.prefix_n = 1;
     c.prefix_r = r;
