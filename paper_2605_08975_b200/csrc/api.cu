@@ -117,6 +117,13 @@ void upload_lane_map(Ctx& c, const alpa_request& r) {
     }
     for (int32_t v : map)
         if (v < 0 || v >= c.prefix_n) fail(ALPA_ERR_CONFIG, "lane prefix index out of range");
+    int64_t uni = map.empty() ? 0 : map[0];
+    for (int32_t v : map)
+        if (v != uni) uni = -1;
+    if (uni != c.uniform_prefix) {
+        c.uniform_prefix = uni;  // selects the attention kernel captured in the graph
+        alpa::invalidate_graph(c);
+    }
     ALPA_CUDA(cudaMemcpyAsync(c.ws.lane_map, map.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice,
                               c.stream));
 }
@@ -333,6 +340,7 @@ int alpa_bind_prefix_device(alpa_ctx* h, const void* kv, int64_t n_prefix, int64
         c->own_prefix = false;
         c->prefix_n = n_prefix;
         c->prefix_r = r;
+        alpa::refresh_prefix_map(*c);
         alpa::invalidate_graph(*c);
     });
 }

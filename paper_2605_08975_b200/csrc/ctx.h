@@ -55,6 +55,7 @@ struct Workspace {
     int* counters = nullptr;   // scratch arrival counters
     int32_t* lane_map = nullptr;  // [N] prefix index per lane
     CUtensorMap tm_x{}, tm_ctx{}, tm_h1{};  // bf16 activation maps (B operand)
+    CUtensorMap tm_qkv{};                   // q | k | v rows, box {64, 128} (attention)
     int tn = 64;                            // token tile
 };
 
@@ -72,7 +73,7 @@ struct KInfo {
 
 struct GraphCache {
     cudaGraphExec_t exec = nullptr;
-    int64_t n = -1, k = -1;
+    int64_t n = -1, k = -1, prefix_id = -2;
     int64_t nodes = 0;
 };
 
@@ -93,6 +94,9 @@ struct Ctx {
     bool own_prefix = false;
     int64_t prefix_n = 0, prefix_r = 0;
     std::vector<int32_t> lane_map_host;  // multi topology
+    int64_t uniform_prefix = 0;          // prefix index shared by every lane, -1 if mixed
+    CUtensorMap tm_pre{};                // 2-D view [n_prefix*B*2*r][kv], box {64, 128}
+    bool tm_pre_valid = false;
 
     Workspace ws;
     GraphCache graph;
@@ -134,6 +138,7 @@ void ensure_workspace(Ctx& c, int64_t n);
 void enqueue_iteration(Ctx& c, int64_t n, cudaStream_t s);  // one diffusion iteration
 void enqueue_rollout(Ctx& c, int64_t n, const float* d_actions, float* d_traj, cudaStream_t s);
 void invalidate_graph(Ctx& c);
+void refresh_prefix_map(Ctx& c);  // TMA map of the bound prefix (bf16)
 
 // tma.cu
 void make_tmap_bf16_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,

@@ -17,6 +17,7 @@
 
 #include "common.cuh"
 #include "ctx.h"
+#include "tc_attn.cuh"
 #include "tc_gemm.cuh"
 
 namespace alpa {
@@ -484,6 +485,37 @@ void gemm_f32(Ctx& c, const char* tag, const Linear& L, const float* A, int64_t 
            (const float*)L.w, L.out, (const float*)L.b, out, ldo, T, (int)L.out, (int)L.in);
 }
 
+template <int HD>
+void launch_attn(Ctx& c, const KInfo& info, int64_t n, int64_t b, cudaStream_t s) {
+    using Cf = AttnCfg<HD>;
+    static bool configured = false;
+    if (!configured) {
+        ALPA_CUDA(cudaFuncSetAttribute(tc_attn_kernel<HD>,
+                                       cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM));
+        configured = true;
+    }
+    const int64_t A = c.steps(), M = n * A, kv = c.kv(), H = c.cfg.heads, r = c.prefix_r;
+    AttnArgs a{};
+    a.M = (int)M;
+    a.r = (int)r;
+    a.kv = (int)kv;
+    a.nbp = (int)((r + 127) / 128);
+    const int qtiles = (int)((M + 127) / 128);
+    const int tiles = (int)H * qtiles;
+    int S = 1;
+    for (int t = 2; t <= 8; ++t)
+        if (t <= a.nbp + 1 && tiles * t <= 148) S = t;
+    if (const char* e = getenv("ALPA_ATTN_SPLITS")) S = std::max(1, std::min(atoi(e), a.nbp + 1));
+    a.splits = S;
+    const int64_t blk = (c.uniform_prefix * c.cfg.decoder_blocks + b) * 2;
+    a.pre_k_row = blk * r;
+    a.pre_v_row = (blk + 1) * r;
+    a.alpha = 1.0f / sqrtf((float)(kv / H));
+    a.ctx = (__nv_bfloat16*)c.ws.ctxb;
+    launch_cl(c, info, dim3(1, 1, S), tc_attn_kernel<HD>, dim3((unsigned)H, (unsigned)qtiles, S),
+              dim3(192), (size_t)Cf::SMEM, s, c.ws.tm_qkv, c.tm_pre, a);
+}
+
 }  // namespace
 
 void ensure_workspace(Ctx& c, int64_t n) {
@@ -514,6 +546,7 @@ void ensure_workspace(Ctx& c, int64_t n) {
         make_tmap_bf16_2d(&w.tm_x, w.x, ah, M, ah * 2, 64, w.tn);
         make_tmap_bf16_2d(&w.tm_ctx, w.ctxb, kv, M, kv * 2, 64, w.tn);
         make_tmap_bf16_2d(&w.tm_h1, w.h1, 4 * ah, M, 4 * ah * 2, 64, w.tn);
+        make_tmap_bf16_2d(&w.tm_qkv, w.qkv, 3 * kv, M, 3 * kv * 2, 64, 128);
     }
 }
 
@@ -545,10 +578,18 @@ void enqueue_iteration(Ctx& c, int64_t n, cudaStream_t s) {
             launch(c, ln, layernorm_kernel<bf>, dim3(ln_grid), dim3(256), 0, s, (const float*)w.e,
                    (bf*)w.x, M, ah);
             gemm_tc<EPI_BF16>(c, "gemm_qkv", blk.qkv, w.tm_x, T, w.qkv, 3 * kv, s);
-            launch(c, att, attn_simt_kernel<bf>, dim3(attn_grid), dim3(256), 0, s,
-                   (const bf*)w.qkv, (const bf*)c.prefix, prefix_stride, b * 2 * r * kv,
-                   (const int32_t*)w.lane_map, (int)n, (int)r, (int)kv, (int)H, (int)A, alpha,
-                   (bf*)w.ctxb);
+            const int64_t hd = kv / H;
+            if (c.uniform_prefix >= 0 && c.tm_pre_valid && (hd == 64 || hd == 128)) {
+                if (hd == 128)
+                    launch_attn<128>(c, att, n, b, s);
+                else
+                    launch_attn<64>(c, att, n, b, s);
+            } else {
+                launch(c, att, attn_simt_kernel<bf>, dim3(attn_grid), dim3(256), 0, s,
+                       (const bf*)w.qkv, (const bf*)c.prefix, prefix_stride, b * 2 * r * kv,
+                       (const int32_t*)w.lane_map, (int)n, (int)r, (int)kv, (int)H, (int)A,
+                       alpha, (bf*)w.ctxb);
+            }
             gemm_tc<EPI_RESID_F32>(c, "gemm_o", blk.o, w.tm_ctx, T, w.e, ah, s);
             launch(c, ln, layernorm_kernel<bf>, dim3(ln_grid), dim3(256), 0, s, (const float*)w.e,
                    (bf*)w.x, M, ah);
@@ -589,6 +630,14 @@ void enqueue_rollout(Ctx& c, int64_t n, const float* d_actions, float* d_traj, c
     launch(c, info, rollout_kernel, dim3((unsigned)((n + 63) / 64)), dim3(64), 0, s, d_actions,
            d_traj,
            (int)n, (int)c.steps(), (const float*)c.d_scalars, bad);
+}
+
+void refresh_prefix_map(Ctx& c) {
+    c.tm_pre_valid = false;
+    if (!c.bf16() || !c.prefix) return;
+    const uint64_t rows = (uint64_t)c.prefix_n * c.cfg.decoder_blocks * 2 * c.prefix_r;
+    make_tmap_bf16_2d(&c.tm_pre, c.prefix, (uint64_t)c.kv(), rows, (uint64_t)c.kv() * 2, 64, 128);
+    c.tm_pre_valid = true;
 }
 
 void invalidate_graph(Ctx& c) {

@@ -232,6 +232,7 @@ void make_prefix_synthetic(Ctx& c, uint64_t seed, int64_t r) {
     ALPA_CUDA(cudaStreamSynchronize(c.stream));
     c.prefix_n = 1;
     c.prefix_r = r;
+    refresh_prefix_map(c);
 }
 
 void make_prefix_from_host(Ctx& c, const float* host, int64_t n_prefix, int64_t r) {
@@ -254,6 +255,7 @@ void make_prefix_from_host(Ctx& c, const float* host, int64_t n_prefix, int64_t 
     }
     c.prefix_n = n_prefix;
     c.prefix_r = r;
+    refresh_prefix_map(c);
 }
 
 }  // namespace alpa

@@ -261,3 +261,22 @@ def test_bf16_small_width(port):
     print(f"bf16 small width rel-L2 {err:.3e}")
     assert err <= BF16_TOL
     np.testing.assert_array_equal(res.actions, res2.actions)  # deterministic split-K
+
+
+@pytest.mark.parametrize("r,splits", [(1000, "1"), (256, "2"), (2048, None)])
+def test_bf16_attention_kv_splits(port, monkeypatch, r, splits):
+    # multi-block online softmax (rescale of the TMEM accumulator) and the
+    # cluster/DSMEM split combine, incl. a prefix length that is not a
+    # multiple of the 128-key block.
+    if splits:
+        monkeypatch.setenv("ALPA_ATTN_SPLITS", splits)
+    B = 1
+    m = c2(B=B, K=1) if r == 2048 else c2(B=B, K=1, action_hidden_dim=256, kv_dim=128, heads=1)
+    pre = port.synthetic_prefix(7, B, r, m.kv_dim)
+    exp = port.refine(ocfg(m), port.weights(ocfg(m)), pre, port.noise(2, 1, 6))
+    with alpa.ActionGenerator(m) as g:
+        g.bind_prefix(pre)
+        res = g.run_action_generation(alpa.InferenceRequest(num_trajectories=6, v0=5.0))
+    err = rel_l2(res.actions, exp)
+    print(f"bf16 attention r={r} splits={splits}: rel-L2 {err:.3e}")
+    assert err <= BF16_TOL
