@@ -24,7 +24,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libalpa_action.so")
+LIB_PATH = os.environ.get("ALPA_LIB") or os.path.join(_HERE, "libalpa_action.so")
 
 ALPA_OK, ALPA_ERR_IO, ALPA_ERR_CONFIG, ALPA_ERR_INTERNAL = 0, 1, 2, 3
 DTYPES = {"f32": 0, "fp32": 0, "float32": 0, "bf16": 1, "bfloat16": 1}

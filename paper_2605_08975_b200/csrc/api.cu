@@ -522,6 +522,7 @@ int alpa_profile(alpa_ctx* h, const alpa_request* req, int64_t iters, alpa_kerne
     });
 }
 
+
 void alpa_host_noise(uint64_t seed, uint64_t stride, int64_t lane0, int64_t n, int64_t steps,
                      float* out) {
     for (int64_t l = 0; l < n; ++l) {

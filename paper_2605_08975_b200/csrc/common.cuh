@@ -235,6 +235,25 @@ __device__ inline float4 ld_dsmem_f4(uint32_t addr) {
     return v;
 }
 
+// Debug-only phase trace (-DALPA_TRACE): globaltimer stamps per CTA.
+#ifdef ALPA_TRACE
+__device__ unsigned long long g_trace[4096][8];
+__device__ inline unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+#define ALPA_STAMP_AT(base, slot)                                                             \
+    do {                                                                                      \
+        const int cta_ = blockIdx.x + gridDim.x * (blockIdx.y + gridDim.y * blockIdx.z);     \
+        if (cta_ < 2048) g_trace[(base) + cta_][slot] = gtimer();                             \
+    } while (0)
+#else
+#define ALPA_STAMP_AT(base, slot) \
+    do {                          \
+    } while (0)
+#endif
+
 // Programmatic dependent launch.
 __device__ inline void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ inline void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;"); }

@@ -36,6 +36,7 @@ struct Linear {
     float* b = nullptr;
     int64_t in = 0, out = 0;
     CUtensorMap tmap{};  // bf16: TMA map of W^T, box {64, 128}
+    float* colsum = nullptr;  // bf16: sum_k W^T[f][k] (LayerNorm fold), LN consumers only
 };
 
 struct Block {
@@ -53,6 +54,7 @@ struct Workspace {
     void* ctxb = nullptr;      // attention output [M][kv]
     void* h1 = nullptr;        // MLP hidden [M][4ah]
     int* counters = nullptr;   // scratch arrival counters
+    float2* stats = nullptr;   // bf16 path: [M][ah/128] (sum, sumsq) of e rows per feature tile
     int32_t* lane_map = nullptr;  // [N] prefix index per lane
     CUtensorMap tm_x{}, tm_ctx{}, tm_h1{};  // bf16 activation maps (B operand)
     CUtensorMap tm_qkv{};                   // q | k | v rows, box {64, 128} (attention)

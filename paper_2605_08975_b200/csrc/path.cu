@@ -429,7 +429,7 @@ TcPlan plan_tc(int nf, int T, int K, int tn) {
     const int tiles = (nf / 128) * ((T + tn - 1) / tn);
     const int KB = K / 64;
     int best = 1;
-    for (int s : {2, 3, 4, 6, 8})
+    for (int s : {2, 4, 8})
         if (tn % s == 0 && tiles * s <= 148 && KB % s == 0 && KB / s >= 2) best = s;
     return {best, KB / best};
 }
@@ -441,9 +441,15 @@ KInfo gemm_info(const char* tag, const Linear& L, int T, size_t esz, int epi) {
     return {tag, 2.0 * T * L.in * L.out, w + x + o};
 }
 
+// LN-fold side channels of one GEMM launch (see tc_gemm.cuh).
+struct Side {
+    bool produce = false;  // write e stats + bf16 copy (residual producers)
+    bool consume = false;  // fold LN of the input rows (QKV, mlp1)
+};
+
 template <int TN, int EPI>
 void launch_tc(Ctx& c, const char* tag, const Linear& L, const CUtensorMap& tmx, int T, void* out,
-               int64_t ldo, cudaStream_t s) {
+               int64_t ldo, cudaStream_t s, Side side = {}) {
     using Cf = GemmCfg<TN>;
     static bool configured = false;
     if (!configured) {
@@ -461,6 +467,16 @@ void launch_tc(Ctx& c, const char* tag, const Linear& L, const CUtensorMap& tmx,
     const TcPlan p = plan_tc(a.nf, T, a.k, TN);
     a.splits = p.splits;
     a.kbs = p.kbs;
+    a.nft = (int)(c.ah() / 128);
+    a.ln_n = (int)c.ah();
+    if (side.produce) {
+        a.stats_out = c.ws.stats;
+        a.xb_out = (__nv_bfloat16*)c.ws.x;
+    }
+    if (side.consume) {
+        a.stats_in = c.ws.stats;
+        a.colsum = L.colsum;
+    }
     dim3 grid(a.nf / 128, (T + TN - 1) / TN, p.splits);
     launch_cl(c, gemm_info(tag, L, T, 2, EPI), dim3(1, 1, p.splits), tc_gemm_kernel<TN, EPI>, grid,
               dim3(192), (size_t)Cf::SMEM, s, L.tmap, tmx, a);
@@ -468,12 +484,12 @@ void launch_tc(Ctx& c, const char* tag, const Linear& L, const CUtensorMap& tmx,
 
 template <int EPI>
 void gemm_tc(Ctx& c, const char* tag, const Linear& L, const CUtensorMap& tmx, int T, void* out,
-             int64_t ldo, cudaStream_t s) {
+             int64_t ldo, cudaStream_t s, Side side = {}) {
     switch (c.ws.tn) {
-        case 64: launch_tc<64, EPI>(c, tag, L, tmx, T, out, ldo, s); break;
-        case 128: launch_tc<128, EPI>(c, tag, L, tmx, T, out, ldo, s); break;
-        case 192: launch_tc<192, EPI>(c, tag, L, tmx, T, out, ldo, s); break;
-        default: launch_tc<256, EPI>(c, tag, L, tmx, T, out, ldo, s); break;
+        case 64: launch_tc<64, EPI>(c, tag, L, tmx, T, out, ldo, s, side); break;
+        case 128: launch_tc<128, EPI>(c, tag, L, tmx, T, out, ldo, s, side); break;
+        case 192: launch_tc<192, EPI>(c, tag, L, tmx, T, out, ldo, s, side); break;
+        default: launch_tc<256, EPI>(c, tag, L, tmx, T, out, ldo, s, side); break;
     }
 }
 
@@ -502,8 +518,10 @@ void launch_attn(Ctx& c, const KInfo& info, int64_t n, int64_t b, cudaStream_t s
     a.nbp = (int)((r + 127) / 128);
     const int qtiles = (int)((M + 127) / 128);
     const int tiles = (int)H * qtiles;
+    // KV splits = cluster size: 2 or 4 (clusters of 3/5/6 do not pack the
+    // 16-20-SM GPCs into one wave), one wave, >= 1 block per split.
     int S = 1;
-    for (int t = 2; t <= 8; ++t)
+    for (int t : {2, 4})
         if (t <= a.nbp + 1 && tiles * t <= 148) S = t;
     if (const char* e = getenv("ALPA_ATTN_SPLITS")) S = std::max(1, std::min(atoi(e), a.nbp + 1));
     a.splits = S;
@@ -524,7 +542,7 @@ void ensure_workspace(Ctx& c, int64_t n) {
     invalidate_graph(c);
     Workspace& w = c.ws;
     for (void* p : {(void*)w.actions, (void*)w.traj, (void*)w.e, w.x, w.qkv, w.ctxb, w.h1,
-                    (void*)w.counters, (void*)w.lane_map})
+                    (void*)w.counters, (void*)w.lane_map, (void*)w.stats})
         if (p) c.dfree(p);
     w = Workspace{};
     const int64_t A = c.steps(), M = n * A, ah = c.ah(), kv = c.kv();
@@ -543,6 +561,7 @@ void ensure_workspace(Ctx& c, int64_t n) {
     const int T = (int)M;
     w.tn = (T % 256 == 0) ? 256 : (T % 192 == 0) ? 192 : (T % 128 == 0) ? 128 : 64;
     if (c.bf16()) {
+        w.stats = (float2*)c.dalloc(M * (ah / 128) * sizeof(float2));
         make_tmap_bf16_2d(&w.tm_x, w.x, ah, M, ah * 2, 64, w.tn);
         make_tmap_bf16_2d(&w.tm_ctx, w.ctxb, kv, M, kv * 2, 64, w.tn);
         make_tmap_bf16_2d(&w.tm_h1, w.h1, 4 * ah, M, 4 * ah * 2, 64, w.tn);
@@ -571,13 +590,16 @@ void enqueue_iteration(Ctx& c, int64_t n, cudaStream_t s) {
         using bf = __nv_bfloat16;
         launch(c, enc, encode_kernel<bf>, dim3(ew_grid(M * ah)), dim3(256), 0, s, w.actions,
                (const float*)c.act_in.w, c.act_in.b, c.pos, (bf*)w.x, M, ah, A);
+        // LayerNorms are folded into the GEMMs: residual producers emit the
+        // bf16 copy of e (into x) + row statistics, QKV / mlp1 consume them.
+        Side prod, cons;
+        prod.produce = true;
+        cons.consume = true;
         gemm_tc<EPI_GELU_BF16>(c, "gemm_enc_mlp1", c.mlp1, w.tm_x, T, w.h1, 4 * ah, s);
-        gemm_tc<EPI_F32>(c, "gemm_enc_mlp2", c.mlp2, w.tm_h1, T, w.e, ah, s);
+        gemm_tc<EPI_F32>(c, "gemm_enc_mlp2", c.mlp2, w.tm_h1, T, w.e, ah, s, prod);
         for (int64_t b = 0; b < c.cfg.decoder_blocks; ++b) {
             const Block& blk = c.blocks[b];
-            launch(c, ln, layernorm_kernel<bf>, dim3(ln_grid), dim3(256), 0, s, (const float*)w.e,
-                   (bf*)w.x, M, ah);
-            gemm_tc<EPI_BF16>(c, "gemm_qkv", blk.qkv, w.tm_x, T, w.qkv, 3 * kv, s);
+            gemm_tc<EPI_LN_BF16>(c, "gemm_qkv", blk.qkv, w.tm_x, T, w.qkv, 3 * kv, s, cons);
             const int64_t hd = kv / H;
             if (c.uniform_prefix >= 0 && c.tm_pre_valid && (hd == 64 || hd == 128)) {
                 if (hd == 128)
@@ -590,11 +612,9 @@ void enqueue_iteration(Ctx& c, int64_t n, cudaStream_t s) {
                        (const int32_t*)w.lane_map, (int)n, (int)r, (int)kv, (int)H, (int)A,
                        alpha, (bf*)w.ctxb);
             }
-            gemm_tc<EPI_RESID_F32>(c, "gemm_o", blk.o, w.tm_ctx, T, w.e, ah, s);
-            launch(c, ln, layernorm_kernel<bf>, dim3(ln_grid), dim3(256), 0, s, (const float*)w.e,
-                   (bf*)w.x, M, ah);
-            gemm_tc<EPI_GELU_BF16>(c, "gemm_mlp1", blk.mlp1, w.tm_x, T, w.h1, 4 * ah, s);
-            gemm_tc<EPI_RESID_F32>(c, "gemm_mlp2", blk.mlp2, w.tm_h1, T, w.e, ah, s);
+            gemm_tc<EPI_RESID_F32>(c, "gemm_o", blk.o, w.tm_ctx, T, w.e, ah, s, prod);
+            gemm_tc<EPI_LN_GELU_BF16>(c, "gemm_mlp1", blk.mlp1, w.tm_x, T, w.h1, 4 * ah, s, cons);
+            gemm_tc<EPI_RESID_F32>(c, "gemm_mlp2", blk.mlp2, w.tm_h1, T, w.e, ah, s, prod);
         }
     } else {
         float* x = (float*)w.x;
@@ -639,6 +659,17 @@ void refresh_prefix_map(Ctx& c) {
     make_tmap_bf16_2d(&c.tm_pre, c.prefix, (uint64_t)c.kv(), rows, (uint64_t)c.kv() * 2, 64, 128);
     c.tm_pre_valid = true;
 }
+
+#ifdef ALPA_TRACE
+// debug builds only: per-CTA phase stamps of the most recent traced kernels
+extern "C" int alpa_debug_trace(unsigned long long* out, int64_t n) {
+    return cudaMemcpyFromSymbol(out, g_trace, sizeof(unsigned long long) * 8 * n) == cudaSuccess ? 0 : 3;
+}
+extern "C" int alpa_debug_trace_clear(void) {
+    static unsigned long long z[4096][8];
+    return cudaMemcpyToSymbol(g_trace, z, sizeof(z)) == cudaSuccess ? 0 : 3;
+}
+#endif
 
 void invalidate_graph(Ctx& c) {
     if (c.graph.exec) cudaGraphExecDestroy(c.graph.exec);

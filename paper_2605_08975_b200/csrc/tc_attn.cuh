@@ -81,6 +81,7 @@ __global__ void __launch_bounds__(192, 1)
     const int g0 = (blockIdx.z * nb) / S, g1 = ((blockIdx.z + 1) * nb) / S;
     const int nj = g1 - g0;
     const int row0 = qt * 128;
+    if (threadIdx.x == 0) ALPA_STAMP_AT(0, 0);
 
     if (threadIdx.x == 0) {
         tma_prefetch(&tmQKV);
@@ -103,6 +104,7 @@ __global__ void __launch_bounds__(192, 1)
     const uint32_t tbase = *tmem_slot;
     const uint32_t tS[2] = {tbase, tbase + 128};
     const uint32_t tO = tbase + 256;
+    if (threadIdx.x == 0) ALPA_STAMP_AT(0, 1);
 
     if (warp == 4) {
         // ------------------------------------------------ TMA producer
@@ -151,6 +153,7 @@ __global__ void __launch_bounds__(192, 1)
             constexpr uint32_t idS = idesc_bf16(128, 128);
             constexpr uint32_t idO = idesc_bf16(128, HD, true);
             mbar_wait(qfull, 0);
+            ALPA_STAMP_AT(0, 2);
             auto issue_s = [&](int j) {
                 const int st = j & 1;
                 mbar_wait(&kvfull[st], (j >> 1) & 1);
@@ -196,6 +199,7 @@ __global__ void __launch_bounds__(192, 1)
         for (int j = 0; j < nj; ++j) {
             const int st = j & 1, g = g0 + j;
             mbar_wait(&sfull[st], (j >> 1) & 1);
+            if (i == 0 && j == 0) ALPA_STAMP_AT(0, 3);
             tc_fence_after();
             uint32_t sr[128];
 #pragma unroll
@@ -288,6 +292,7 @@ __global__ void __launch_bounds__(192, 1)
             for (int c = 0; c < HD; c += 4)
                 *reinterpret_cast<float4*>(stage + i * C::O_STRIDE + c) = make_float4(0.f, 0.f, 0.f, 0.f);
         }
+        if (i == 0) ALPA_STAMP_AT(0, 4);
         m_sh[i] = m;  // log2 domain (alpha*log2e folded in)
         l_sh[i] = l;
     }
@@ -295,52 +300,80 @@ __global__ void __launch_bounds__(192, 1)
     __syncthreads();
     pdl_launch();
     // ------------------------------------------------ split combine + store (all warps)
+    // CTA `rank` of the cluster owns rows [rank*128/S, (rank+1)*128/S).  Phase
+    // 1 gathers every split's (m, l) for those rows (independent DSMEM loads),
+    // phase 2 turns them into per-split weights w_s / L in local smem, phase 3
+    // streams the O partials with all S loads of an item in flight.
     {
         const uint32_t rank = S > 1 ? cluster_ctarank() : 0;
         if (S > 1) cluster_sync_all();
+        ALPA_STAMP_AT(0, 5);
         const int r_begin = (int)(rank * 128) / S, r_end = (int)((rank + 1) * 128) / S;
+        const int rows = r_end - r_begin;
         const uint32_t st_local = smem_u32(smem + C::OFF_KV);
         const uint32_t m_local = smem_u32(m_sh), l_local = smem_u32(l_sh);
-        constexpr int LPR = HD / 4;            // lanes (float4 columns) per row
-        constexpr int RPW = 32 / LPR;          // rows per warp pass
-        const int sub = lane / LPR, cq = (lane % LPR) * 4;
-        for (int rr = r_begin + warp * RPW + sub; rr < r_end; rr += 6 * RPW) {
-            float ms[8], ws[8];
+        float* wgt = reinterpret_cast<float*>(smem + C::OFF_P);  // [S][rows] (P ring is free)
+        float* gm = wgt + 8 * 128;                                // [S][rows] gathered m
+        float* gl = gm + 8 * 128;                                 // [S][rows] gathered l
+        for (int t = threadIdx.x; t < S * rows; t += 192) {
+            const int s2 = t / rows, rr = r_begin + t % rows;
+            float mv, lv;
+            const uint32_t ma = (S > 1 ? dsmem_addr(m_local, s2) : m_local) + rr * 4;
+            const uint32_t la = (S > 1 ? dsmem_addr(l_local, s2) : l_local) + rr * 4;
+            asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(mv) : "r"(ma) : "memory");
+            asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(lv) : "r"(la) : "memory");
+            gm[t] = mv;
+            gl[t] = lv;
+        }
+        __syncthreads();
+        for (int rl = threadIdx.x; rl < rows; rl += 192) {
             float M = -INFINITY;
-            for (int s2 = 0; s2 < S; ++s2) {
-                float v;
-                const uint32_t addr = (S > 1 ? dsmem_addr(m_local, s2) : m_local) + rr * 4;
-                asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(addr) : "memory");
-                ms[s2] = v;
-                M = fmaxf(M, v);
-            }
+            for (int s2 = 0; s2 < S; ++s2) M = fmaxf(M, gm[s2 * rows + rl]);
             float L = 0.f;
-            float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
             for (int s2 = 0; s2 < S; ++s2) {
-                ws[s2] = ms[s2] == -INFINITY ? 0.f : ex2(ms[s2] - M);
-                float lv;
-                const uint32_t la = (S > 1 ? dsmem_addr(l_local, s2) : l_local) + rr * 4;
-                asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(lv) : "r"(la) : "memory");
-                L += ws[s2] * lv;
-                const uint32_t oa = (S > 1 ? dsmem_addr(st_local, s2) : st_local) +
-                                    (uint32_t)(rr * C::O_STRIDE + cq) * 4u;
-                const float4 p = ld_dsmem_f4(oa);
-                o.x += ws[s2] * p.x; o.y += ws[s2] * p.y; o.z += ws[s2] * p.z; o.w += ws[s2] * p.w;
+                const float mv = gm[s2 * rows + rl];
+                const float w = mv == -INFINITY ? 0.f : ex2(mv - M);
+                wgt[s2 * rows + rl] = w;
+                L += w * gl[s2 * rows + rl];
             }
+            const float inv = 1.0f / L;
+            for (int s2 = 0; s2 < S; ++s2) wgt[s2 * rows + rl] *= inv;
+        }
+        __syncthreads();
+        constexpr int CG = HD / 4;  // float4 column groups per row
+        uint32_t base[8];
+#pragma unroll
+        for (int s2 = 0; s2 < 8; ++s2) base[s2] = (s2 < S && S > 1) ? dsmem_addr(st_local, s2) : st_local;
+        for (int it = threadIdx.x; it < rows * CG; it += 192) {
+            const int rl = it / CG, cq = (it % CG) * 4;
+            const int rr = r_begin + rl;
+            const uint32_t off = (uint32_t)(rr * C::O_STRIDE + cq) * 4u;
+            float4 p[8];
+#pragma unroll
+            for (int s2 = 0; s2 < 8; ++s2)
+                if (s2 < S) p[s2] = ld_dsmem_f4(base[s2] + off);
+            float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int s2 = 0; s2 < 8; ++s2)
+                if (s2 < S) {
+                    const float w = wgt[s2 * rows + rl];
+                    o.x += w * p[s2].x; o.y += w * p[s2].y; o.z += w * p[s2].z; o.w += w * p[s2].w;
+                }
             const int t = row0 + rr;
             if (t < a.M) {
-                const float inv = 1.0f / L;
-                __nv_bfloat162 lo2 = __floats2bfloat162_rn(o.x * inv, o.y * inv);
-                __nv_bfloat162 hi2 = __floats2bfloat162_rn(o.z * inv, o.w * inv);
+                __nv_bfloat162 lo2 = __floats2bfloat162_rn(o.x, o.y);
+                __nv_bfloat162 hi2 = __floats2bfloat162_rn(o.z, o.w);
                 uint2 pk;
                 pk.x = *reinterpret_cast<uint32_t*>(&lo2);
                 pk.y = *reinterpret_cast<uint32_t*>(&hi2);
-                *reinterpret_cast<uint2*>(a.ctx + (int64_t)t * a.kv + h * HD + cq) = pk;
+                *reinterpret_cast<uint2*>(a.ctx + (int64_t)t * a.kv + blockIdx.x * HD + cq) = pk;
             }
         }
+        ALPA_STAMP_AT(0, 6);
         if (S > 1) cluster_sync_all();
     }
     if (warp == 5) tmem_dealloc(tbase, 512);
+    if (threadIdx.x == 160) ALPA_STAMP_AT(0, 7);
 }
 
 }  // namespace alpa

@@ -35,7 +35,15 @@ enum Epi : int {
     EPI_F32 = 2,        // out f32  = acc + b                      (encoder mlp2, model.cpp:562)
     EPI_RESID_F32 = 3,  // out f32  = out + (acc + b)              (o / mlp2 + residual, model.cpp:582-588)
     EPI_NONE = 4,       // benchmarking only: accumulator discarded
+    EPI_LN_BF16 = 5,    // out bf16 = rstd*(acc - mu*colsum) + b   (LN1 folded into QKV)
+    EPI_LN_GELU_BF16 = 6,  // out bf16 = gelu(rstd*(acc - mu*colsum) + b)  (LN2 folded into mlp1)
 };
+// LayerNorm fold (gamma = 1, beta = 0, model.cpp:83-88): with x = bf16(e),
+//   LN(e).W = rstd * (x.W - mu * colsum(W)),  colsum(W)[f] = sum_k W[f][k].
+// The residual-producing GEMMs (EPI_F32 / EPI_RESID_F32) emit, next to the
+// fp32 stream e, its bf16 copy and per-(row, 128-feature tile) partial
+// (sum, sum of squares); the consumer reduces the tile partials of its rows in
+// a fixed order (deterministic) to mu and rstd = 1/sqrt(var + 1e-5).
 
 struct GemmArgs {
     int nf, t, k;          // features (MMA M), tokens (MMA N), reduction
@@ -43,6 +51,13 @@ struct GemmArgs {
     void* out;             // [t][ldo]
     int64_t ldo;
     int splits, kbs;       // split-K count (= cluster size along z), k-blocks per split
+    // LN fold side channels
+    float2* stats_out;             // [t][nft] (sum, sumsq) of the new e rows, or null
+    __nv_bfloat16* xb_out;         // [t][nf]  bf16 copy of the new e rows, or null
+    const float2* stats_in;        // [t][nft] partials of the LN input rows
+    const float* colsum;           // [nf] column sums of the bf16 weights
+    int nft;                       // feature tiles per stats row
+    int ln_n;                      // LayerNorm width
 };
 
 template <int TN>
@@ -94,6 +109,7 @@ __global__ void __launch_bounds__(192, 1)
     const int KB = a.k / 64;
     const int kb0 = blockIdx.z * a.kbs;
     const int nkb = min(KB, kb0 + a.kbs) - kb0;
+    if (threadIdx.x == 0) ALPA_STAMP_AT(2048, 0);
 
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmW);
@@ -110,6 +126,7 @@ __global__ void __launch_bounds__(192, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tbase = *tmem_slot;
+    if (threadIdx.x == 0) ALPA_STAMP_AT(2048, 1);
 
     if (warp == 0) {
         if (lane == 0) {
@@ -140,6 +157,7 @@ __global__ void __launch_bounds__(192, 1)
                 const int st = i % C::STAGES;
                 const uint32_t ph = (i / C::STAGES) & 1;
                 mbar_wait(&full[st], ph);
+                if (i == 0) ALPA_STAMP_AT(2048, 2);
                 tc_fence_after();
                 uint8_t* sw = smem + st * C::STAGE;
                 const uint64_t da = sdesc_k_sw128(sw);
@@ -158,6 +176,7 @@ __global__ void __launch_bounds__(192, 1)
         const uint32_t trow = tbase + (uint32_t(q * 32) << 16);
         float* stage = reinterpret_cast<float*>(smem);  // [TN][128] fp32
         mbar_wait(accf, 0);
+        if (threadIdx.x == 64) ALPA_STAMP_AT(2048, 3);
         tc_fence_after();
         const int fl = q * 32 + lane;
 #pragma unroll 1
@@ -177,36 +196,106 @@ __global__ void __launch_bounds__(192, 1)
         const int S = a.splits;
         const int rows = TN / S;
         const uint32_t rank = S > 1 ? cluster_ctarank() : 0;
+        if (threadIdx.x == 0) ALPA_STAMP_AT(2048, 4);
         if (S > 1) cluster_sync_all();  // every split staged its partial
+        if (threadIdx.x == 0) ALPA_STAMP_AT(2048, 5);
         const int r0 = (int)rank * rows;
         const int fq = (threadIdx.x & 31) * 4;        // 4 features per lane
         const float4 b4 = *reinterpret_cast<const float4*>(a.bias + f0 + fq);
         const uint32_t stage_base = smem_u32(smem);
         uint32_t src[8];
-        for (int s2 = 0; s2 < S; ++s2) src[s2] = S > 1 ? dsmem_addr(stage_base, s2) : stage_base;
+#pragma unroll
+        for (int s2 = 0; s2 < 8; ++s2) src[s2] = (s2 < S && S > 1) ? dsmem_addr(stage_base, s2) : stage_base;
         pdl_wait();  // residual / outputs may be touched by the previous kernel
-#pragma unroll 2
-        for (int rr = threadIdx.x >> 5; rr < rows; rr += 6) {
-            const int tl = r0 + rr;
-            const int t = t0 + tl;
-            const uint32_t off = (uint32_t)(tl * 128 + fq) * 4u;
-            float4 acc;
-            if (S > 1) {
-                acc = ld_dsmem_f4(src[0] + off);
-                for (int s2 = 1; s2 < S; ++s2) {
-                    const float4 p = ld_dsmem_f4(src[s2] + off);
-                    acc.x += p.x; acc.y += p.y; acc.z += p.z; acc.w += p.w;
+        float4 c4 = make_float4(0.f, 0.f, 0.f, 0.f);
+        if constexpr (EPI == EPI_LN_BF16 || EPI == EPI_LN_GELU_BF16)
+            c4 = *reinterpret_cast<const float4*>(a.colsum + f0 + fq);
+        const int lane32 = threadIdx.x & 31;
+        // 4 rows per pass, every DSMEM / global load of the pass in flight at once
+        for (int rb = threadIdx.x >> 5; rb < rows; rb += 24) {
+            float4 acc[4];
+            float4 res[4];
+            float2 st[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int tl = r0 + rb + 6 * u;
+                acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+                res[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+                st[u] = make_float2(0.f, 0.f);
+                if (rb + 6 * u >= rows) continue;
+                const uint32_t off = (uint32_t)(tl * 128 + fq) * 4u;
+                if (S > 1) {
+                    float4 p[8];
+#pragma unroll
+                    for (int s2 = 0; s2 < 8; ++s2)
+                        if (s2 < S) p[s2] = ld_dsmem_f4(src[s2] + off);
+#pragma unroll
+                    for (int s2 = 0; s2 < 8; ++s2)
+                        if (s2 < S) {
+                            acc[u].x += p[s2].x; acc[u].y += p[s2].y;
+                            acc[u].z += p[s2].z; acc[u].w += p[s2].w;
+                        }
+                } else {
+                    acc[u] = *reinterpret_cast<const float4*>(smem + off);
                 }
-            } else {
-                acc = *reinterpret_cast<const float4*>(smem + off);
+                const int t = t0 + tl;
+                if (t < a.t) {
+                    if constexpr (EPI == EPI_RESID_F32)
+                        res[u] = *reinterpret_cast<const float4*>(
+                            reinterpret_cast<const float*>(a.out) + (int64_t)t * a.ldo + f0 + fq);
+                    if constexpr (EPI == EPI_LN_BF16 || EPI == EPI_LN_GELU_BF16)
+                        if (lane32 < a.nft) st[u] = a.stats_in[(int64_t)t * a.nft + lane32];
+                }
             }
-            if (t < a.t)
-                epi_store4<EPI>(a, t, f0 + fq,
-                                make_float4(acc.x + b4.x, acc.y + b4.y, acc.z + b4.z, acc.w + b4.w));
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int tl = r0 + rb + 6 * u;
+                const int t = t0 + tl;
+                const bool live = rb + 6 * u < rows && t < a.t;  // warp-uniform
+                if (!live) continue;
+                float4 v = make_float4(acc[u].x + b4.x, acc[u].y + b4.y, acc[u].z + b4.z,
+                                       acc[u].w + b4.w);
+                if constexpr (EPI == EPI_LN_BF16 || EPI == EPI_LN_GELU_BF16) {
+                    const float s1 = warp_sum(st[u].x), s2 = warp_sum(st[u].y);
+                    const float inv_n = 1.0f / (float)a.ln_n;
+                    const float mu = s1 * inv_n;
+                    const float var = fmaxf(s2 * inv_n - mu * mu, 0.f);
+                    const float rstd = 1.0f / sqrtf(var + 1e-5f);
+                    v = make_float4(rstd * (acc[u].x - mu * c4.x) + b4.x,
+                                    rstd * (acc[u].y - mu * c4.y) + b4.y,
+                                    rstd * (acc[u].z - mu * c4.z) + b4.z,
+                                    rstd * (acc[u].w - mu * c4.w) + b4.w);
+                }
+                if constexpr (EPI == EPI_RESID_F32 || EPI == EPI_F32) {
+                    float4 e = v;
+                    if constexpr (EPI == EPI_RESID_F32)
+                        e = make_float4(res[u].x + v.x, res[u].y + v.y, res[u].z + v.z, res[u].w + v.w);
+                    *reinterpret_cast<float4*>(reinterpret_cast<float*>(a.out) + (int64_t)t * a.ldo +
+                                               f0 + fq) = e;
+                    if (a.stats_out) {
+                        const float ps = warp_sum(e.x + e.y + e.z + e.w);
+                        const float pq = warp_sum(e.x * e.x + e.y * e.y + e.z * e.z + e.w * e.w);
+                        if (lane32 == 0) a.stats_out[(int64_t)t * a.nft + blockIdx.x] = make_float2(ps, pq);
+                        __nv_bfloat162 lo = __floats2bfloat162_rn(e.x, e.y), hi = __floats2bfloat162_rn(e.z, e.w);
+                        uint2 pk;
+                        pk.x = *reinterpret_cast<uint32_t*>(&lo);
+                        pk.y = *reinterpret_cast<uint32_t*>(&hi);
+                        *reinterpret_cast<uint2*>(a.xb_out + (int64_t)t * a.ldo + f0 + fq) = pk;
+                    }
+                } else if constexpr (EPI == EPI_LN_BF16) {
+                    epi_store4<EPI_BF16>(a, t, f0 + fq, v);
+                } else if constexpr (EPI == EPI_LN_GELU_BF16) {
+                    epi_store4<EPI_GELU_BF16>(a, t, f0 + fq, v);
+                } else {
+                    epi_store4<EPI>(a, t, f0 + fq, v);
+                }
+            }
         }
+        if (threadIdx.x == 0) ALPA_STAMP_AT(2048, 6);
         if (S > 1) cluster_sync_all();  // keep smem alive until every CTA read it
     }
     if (warp == 1) tmem_dealloc(tbase, C::TCOLS);
+    if (threadIdx.x == 32) ALPA_STAMP_AT(2048, 7);
 }
 
 }  // namespace alpa

@@ -94,6 +94,18 @@ __global__ void synth_prefix(uint64_t seed, int64_t blocks, int64_t r, int64_t k
     }
 }
 
+// colsum[f] = sum_k W^T[f][k] over the bf16-rounded weights (LN fold).
+__global__ void row_sums_bf16(const __nv_bfloat16* __restrict__ w, int64_t rows, int64_t k,
+                              float* __restrict__ out) {
+    const int64_t row = blockIdx.x * (int64_t)(blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (row >= rows) return;
+    float s = 0.f;
+    for (int64_t j = lane; j < k; j += 32) s += __bfloat162float(w[row * k + j]);
+    s = warp_sum(s);
+    if (lane == 0) out[row] = s;
+}
+
 __global__ void f32_to_bf16(const float* in, __nv_bfloat16* out, int64_t n) {
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < n;
          t += (int64_t)gridDim.x * blockDim.x)
@@ -181,8 +193,15 @@ void load_weights(Ctx& c, const float* host_arena, int64_t count, uint64_t seed,
         };
         map(c.mlp1);
         map(c.mlp2);
+        auto colsum = [&](Linear& L) {
+            L.colsum = (float*)c.dalloc(L.out * sizeof(float));
+            row_sums_bf16<<<(unsigned)((L.out + 7) / 8), 256, 0, s>>>((const __nv_bfloat16*)L.w,
+                                                                      L.out, L.in, L.colsum);
+        };
         for (auto& blk : c.blocks) {
             map(blk.qkv); map(blk.o); map(blk.mlp1); map(blk.mlp2);
+            colsum(blk.qkv);
+            colsum(blk.mlp1);
         }
     }
 
