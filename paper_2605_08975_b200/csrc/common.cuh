@@ -254,6 +254,16 @@ __device__ inline unsigned long long gtimer() {
     } while (0)
 #endif
 
+// TMA bulk copy: local smem -> smem of another CTA of the cluster, completing
+// (complete_tx) on the destination CTA's mbarrier.
+__device__ inline void bulk_copy_to_cluster(uint32_t dst_cluster_addr, uint32_t src_cta_addr,
+                                            uint32_t bytes, uint32_t bar_cluster_addr) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(dst_cluster_addr), "r"(src_cta_addr), "r"(bytes), "r"(bar_cluster_addr)
+        : "memory");
+}
+
 // Programmatic dependent launch.
 __device__ inline void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ inline void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;"); }

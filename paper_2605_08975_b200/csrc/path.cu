@@ -429,8 +429,14 @@ TcPlan plan_tc(int nf, int T, int K, int tn) {
     const int tiles = (nf / 128) * ((T + tn - 1) / tn);
     const int KB = K / 64;
     int best = 1;
+    // the split-K epilogue stages TN x 128 fp32 plus (S-1) received slices
+    // in the drained pipeline ring
+    const int stage_bytes = 128 * 64 * 2 + tn * 64 * 2;
+    const int ring = std::min(8, (200 * 1024) / stage_bytes) * stage_bytes;
     for (int s : {2, 4, 8})
-        if (tn % s == 0 && tiles * s <= 148 && KB % s == 0 && KB / s >= 2) best = s;
+        if (tn % s == 0 && tiles * s <= 148 && KB % s == 0 && KB / s >= 2 &&
+            tn * 512 + (s - 1) * (tn / s) * 512 <= ring)
+            best = s;
     return {best, KB / best};
 }
 

@@ -20,9 +20,11 @@
 // accesses along the feature dimension.
 //
 // Split-K is deterministic and on-chip: the S CTAs that share an output tile
-// form one thread-block cluster (1,1,S); after staging, CTA s reduces token
-// rows [s*TN/S, (s+1)*TN/S) by reading all S staged partials through DSMEM in
-// split order, then applies the fused epilogue for those rows.
+// form one thread-block cluster (1,1,S).  CTA s owns token rows
+// [s*TN/S, (s+1)*TN/S): after staging, every CTA pushes each other owner's row
+// slice into that owner's receive slots with one TMA bulk copy
+// (smem -> DSMEM, completing on the owner's mbarrier); the owner then sums the
+// S slices from LOCAL smem in split order and applies the fused epilogue.
 #pragma once
 
 #include "common.cuh"
@@ -102,7 +104,8 @@ __global__ void __launch_bounds__(192, 1)
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
     uint64_t* empty = full + C::STAGES;
     uint64_t* accf = empty + C::STAGES;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(accf + 1);
+    uint64_t* recvb = accf + 1;  // split-K receive barrier
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(recvb + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int f0 = blockIdx.x * 128, t0 = blockIdx.y * TN;
@@ -119,6 +122,7 @@ __global__ void __launch_bounds__(192, 1)
             mbar_init(&empty[i], 1);
         }
         mbar_init(accf, 1);
+        mbar_init(recvb, 1);
         fence_mbar_init();
     }
     if (warp == 1) tmem_alloc(tmem_slot, C::TCOLS);
@@ -196,16 +200,29 @@ __global__ void __launch_bounds__(192, 1)
         const int S = a.splits;
         const int rows = TN / S;
         const uint32_t rank = S > 1 ? cluster_ctarank() : 0;
+        float* stage = reinterpret_cast<float*>(smem);
+        float* recv = stage + TN * 128;  // (S-1) slots of [rows][128]
+        const uint32_t slice_bytes = (uint32_t)rows * 512u;
+        if (S > 1 && threadIdx.x == 0) mbar_expect_tx(recvb, (uint32_t)(S - 1) * slice_bytes);
         if (threadIdx.x == 0) ALPA_STAMP_AT(2048, 4);
-        if (S > 1) cluster_sync_all();  // every split staged its partial
+        if (S > 1) cluster_sync_all();  // every split staged; receive slots are free
         if (threadIdx.x == 0) ALPA_STAMP_AT(2048, 5);
+        if (S > 1) {
+            if (threadIdx.x == 0) {
+                const uint32_t recv_local = smem_u32(recv), bar_local = smem_u32(recvb);
+                for (int d = 0; d < S; ++d) {
+                    if (d == (int)rank) continue;
+                    const int slot = (int)rank < d ? (int)rank : (int)rank - 1;
+                    bulk_copy_to_cluster(dsmem_addr(recv_local + slot * slice_bytes, d),
+                                         smem_u32(stage + d * rows * 128), slice_bytes,
+                                         dsmem_addr(bar_local, d));
+                }
+            }
+            mbar_wait(recvb, 0);
+        }
         const int r0 = (int)rank * rows;
         const int fq = (threadIdx.x & 31) * 4;        // 4 features per lane
         const float4 b4 = *reinterpret_cast<const float4*>(a.bias + f0 + fq);
-        const uint32_t stage_base = smem_u32(smem);
-        uint32_t src[8];
-#pragma unroll
-        for (int s2 = 0; s2 < 8; ++s2) src[s2] = (s2 < S && S > 1) ? dsmem_addr(stage_base, s2) : stage_base;
         pdl_wait();  // residual / outputs may be touched by the previous kernel
         float4 c4 = make_float4(0.f, 0.f, 0.f, 0.f);
         if constexpr (EPI == EPI_LN_BF16 || EPI == EPI_LN_GELU_BF16)
@@ -225,16 +242,15 @@ __global__ void __launch_bounds__(192, 1)
                 if (rb + 6 * u >= rows) continue;
                 const uint32_t off = (uint32_t)(tl * 128 + fq) * 4u;
                 if (S > 1) {
-                    float4 p[8];
-#pragma unroll
-                    for (int s2 = 0; s2 < 8; ++s2)
-                        if (s2 < S) p[s2] = ld_dsmem_f4(src[s2] + off);
-#pragma unroll
-                    for (int s2 = 0; s2 < 8; ++s2)
-                        if (s2 < S) {
-                            acc[u].x += p[s2].x; acc[u].y += p[s2].y;
-                            acc[u].z += p[s2].z; acc[u].w += p[s2].w;
-                        }
+                    // fixed split order 0..S-1: own slice from staging, others from slots
+                    const int rl = rb + 6 * u;
+                    for (int s2 = 0; s2 < S; ++s2) {
+                        const float* src = s2 == (int)rank
+                                               ? stage + tl * 128
+                                               : recv + ((s2 < (int)rank ? s2 : s2 - 1) * rows + rl) * 128;
+                        const float4 p = *reinterpret_cast<const float4*>(src + fq);
+                        acc[u].x += p.x; acc[u].y += p.y; acc[u].z += p.z; acc[u].w += p.w;
+                    }
                 } else {
                     acc[u] = *reinterpret_cast<const float4*>(smem + off);
                 }
