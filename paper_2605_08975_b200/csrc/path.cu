@@ -14,6 +14,7 @@
 // residual stream, fp32 LN/softmax statistics.
 #include <algorithm>
 #include <cstdio>
+#include <cstring>
 
 #include "common.cuh"
 #include "ctx.h"
@@ -451,6 +452,8 @@ KInfo gemm_info(const char* tag, const Linear& L, int T, size_t esz, int epi) {
 struct Side {
     bool produce = false;  // write e stats + bf16 copy (residual producers)
     bool consume = false;  // fold LN of the input rows (QKV, mlp1)
+    const void* pf = nullptr;  // next op's weights to prefetch into L2
+    long long pf_bytes = 0;
 };
 
 template <int TN, int EPI>
@@ -474,6 +477,10 @@ void launch_tc(Ctx& c, const char* tag, const Linear& L, const CUtensorMap& tmx,
     a.splits = p.splits;
     a.kbs = p.kbs;
     a.nft = (int)(c.ah() / 128);
+    {
+        static const char* want = getenv("ALPA_TRACE_TAG");
+        a.trace = want ? (strcmp(want, tag) == 0) : 1;
+    }
     a.ln_n = (int)c.ah();
     if (side.produce) {
         a.stats_out = c.ws.stats;
@@ -483,9 +490,11 @@ void launch_tc(Ctx& c, const char* tag, const Linear& L, const CUtensorMap& tmx,
         a.stats_in = c.ws.stats;
         a.colsum = L.colsum;
     }
+    a.pf_ptr = side.pf;
+    a.pf_bytes = side.pf_bytes;
     dim3 grid(a.nf / 128, (T + TN - 1) / TN, p.splits);
     launch_cl(c, gemm_info(tag, L, T, 2, EPI), dim3(1, 1, p.splits), tc_gemm_kernel<TN, EPI>, grid,
-              dim3(192), (size_t)Cf::SMEM, s, L.tmap, tmx, a);
+              dim3(Cf::THREADS), (size_t)Cf::SMEM, s, L.tmap, tmx, a);
 }
 
 template <int EPI>
@@ -508,7 +517,8 @@ void gemm_f32(Ctx& c, const char* tag, const Linear& L, const float* A, int64_t 
 }
 
 template <int HD>
-void launch_attn(Ctx& c, const KInfo& info, int64_t n, int64_t b, cudaStream_t s) {
+void launch_attn(Ctx& c, const KInfo& info, int64_t n, int64_t b, cudaStream_t s,
+                 const void* pf = nullptr, long long pf_bytes = 0) {
     using Cf = AttnCfg<HD>;
     static bool configured = false;
     if (!configured) {
@@ -536,6 +546,8 @@ void launch_attn(Ctx& c, const KInfo& info, int64_t n, int64_t b, cudaStream_t s
     a.pre_v_row = (blk + 1) * r;
     a.alpha = 1.0f / sqrtf((float)(kv / H));
     a.ctx = (__nv_bfloat16*)c.ws.ctxb;
+    a.pf_ptr = pf;
+    a.pf_bytes = pf_bytes;
     launch_cl(c, info, dim3(1, 1, S), tc_attn_kernel<HD>, dim3((unsigned)H, (unsigned)qtiles, S),
               dim3(192), (size_t)Cf::SMEM, s, c.ws.tm_qkv, c.tm_pre, a);
 }
@@ -598,29 +610,53 @@ void enqueue_iteration(Ctx& c, int64_t n, cudaStream_t s) {
                (const float*)c.act_in.w, c.act_in.b, c.pos, (bf*)w.x, M, ah, A);
         // LayerNorms are folded into the GEMMs: residual producers emit the
         // bf16 copy of e (into x) + row statistics, QKV / mlp1 consume them.
-        Side prod, cons;
-        prod.produce = true;
-        cons.consume = true;
-        gemm_tc<EPI_GELU_BF16>(c, "gemm_enc_mlp1", c.mlp1, w.tm_x, T, w.h1, 4 * ah, s);
-        gemm_tc<EPI_F32>(c, "gemm_enc_mlp2", c.mlp2, w.tm_h1, T, w.e, ah, s, prod);
-        for (int64_t b = 0; b < c.cfg.decoder_blocks; ++b) {
+        // Every op also prefetches the NEXT op's weights (or this block's
+        // prefix K/V for the attention) into L2 while it computes.
+        const int64_t B = c.cfg.decoder_blocks;
+        auto wbytes = [](const Linear& L) { return (long long)(L.in * L.out * 2); };
+        auto side = [&](bool prod, bool cons, const void* pf, long long nb) {
+            Side sd;
+            sd.produce = prod;
+            sd.consume = cons;
+            sd.pf = pf;
+            sd.pf_bytes = nb;
+            return sd;
+        };
+        const int64_t pre_block = 2 * r * kv * 2;  // K + V of one block, bf16
+        auto prefix_of = [&](int64_t b) {
+            return (const void*)((const uint8_t*)c.prefix +
+                                 (c.uniform_prefix < 0 ? 0 : c.uniform_prefix) *
+                                     c.cfg.decoder_blocks * pre_block +
+                                 b * pre_block);
+        };
+        gemm_tc<EPI_GELU_BF16>(c, "gemm_enc_mlp1", c.mlp1, w.tm_x, T, w.h1, 4 * ah, s,
+                               side(false, false, c.mlp2.w, wbytes(c.mlp2)));
+        gemm_tc<EPI_F32>(c, "gemm_enc_mlp2", c.mlp2, w.tm_h1, T, w.e, ah, s,
+                         side(true, false, c.blocks[0].qkv.w, wbytes(c.blocks[0].qkv)));
+        for (int64_t b = 0; b < B; ++b) {
             const Block& blk = c.blocks[b];
-            gemm_tc<EPI_LN_BF16>(c, "gemm_qkv", blk.qkv, w.tm_x, T, w.qkv, 3 * kv, s, cons);
+            gemm_tc<EPI_LN_BF16>(c, "gemm_qkv", blk.qkv, w.tm_x, T, w.qkv, 3 * kv, s,
+                                 side(false, true, prefix_of(b), pre_block));
             const int64_t hd = kv / H;
             if (c.uniform_prefix >= 0 && c.tm_pre_valid && (hd == 64 || hd == 128)) {
                 if (hd == 128)
-                    launch_attn<128>(c, att, n, b, s);
+                    launch_attn<128>(c, att, n, b, s, blk.o.w, wbytes(blk.o));
                 else
-                    launch_attn<64>(c, att, n, b, s);
+                    launch_attn<64>(c, att, n, b, s, blk.o.w, wbytes(blk.o));
             } else {
                 launch(c, att, attn_simt_kernel<bf>, dim3(attn_grid), dim3(256), 0, s,
                        (const bf*)w.qkv, (const bf*)c.prefix, prefix_stride, b * 2 * r * kv,
                        (const int32_t*)w.lane_map, (int)n, (int)r, (int)kv, (int)H, (int)A,
                        alpha, (bf*)w.ctxb);
             }
-            gemm_tc<EPI_RESID_F32>(c, "gemm_o", blk.o, w.tm_ctx, T, w.e, ah, s, prod);
-            gemm_tc<EPI_LN_GELU_BF16>(c, "gemm_mlp1", blk.mlp1, w.tm_x, T, w.h1, 4 * ah, s, cons);
-            gemm_tc<EPI_RESID_F32>(c, "gemm_mlp2", blk.mlp2, w.tm_h1, T, w.e, ah, s, prod);
+            gemm_tc<EPI_RESID_F32>(c, "gemm_o", blk.o, w.tm_ctx, T, w.e, ah, s,
+                                   side(true, false, blk.mlp1.w, wbytes(blk.mlp1)));
+            gemm_tc<EPI_LN_GELU_BF16>(c, "gemm_mlp1", blk.mlp1, w.tm_x, T, w.h1, 4 * ah, s,
+                                      side(false, true, blk.mlp2.w, wbytes(blk.mlp2)));
+            const bool last = b + 1 == B;
+            gemm_tc<EPI_RESID_F32>(c, "gemm_mlp2", blk.mlp2, w.tm_h1, T, w.e, ah, s,
+                                   side(true, false, last ? nullptr : c.blocks[b + 1].qkv.w,
+                                        last ? 0 : wbytes(c.blocks[b + 1].qkv)));
         }
     } else {
         float* x = (float*)w.x;

@@ -37,6 +37,8 @@ struct AttnArgs {
     long long pre_v_row;   // row of (block b, V, token 0)
     float alpha;           // 1/sqrt(head_dim)
     __nv_bfloat16* ctx;    // [M][kv]
+    const void* pf_ptr;    // next op's weights: L2 prefetch, split over the grid
+    long long pf_bytes;
 };
 
 template <int HD>
@@ -60,8 +62,9 @@ __global__ void __launch_bounds__(192, 1)
                    const AttnArgs a) {
     using C = AttnCfg<HD>;
     extern __shared__ uint8_t smem_raw[];
-    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                               ~uintptr_t(1023));
+    // 1024-B aligned (SWIZZLE_128B atoms); offset arithmetic on smem_raw keeps
+    // the shared address space visible to the compiler (LDS/STS, not generic)
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
     uint64_t* qfull = bars + 0;
     uint64_t* kvfull = bars + 1;   // [2]
@@ -130,6 +133,17 @@ __global__ void __launch_bounds__(192, 1)
                     }
                 }
             };
+            if (a.pf_bytes > 0) {
+                const long long ncta = (long long)gridDim.x * gridDim.y * gridDim.z;
+                const long long cta = blockIdx.x + gridDim.x * (blockIdx.y + (long long)gridDim.y * blockIdx.z);
+                const long long chunk = ((a.pf_bytes + ncta - 1) / ncta + 15) & ~15ll;
+                const long long beg = cta * chunk;
+                const long long end = beg + chunk < a.pf_bytes ? beg + chunk : a.pf_bytes;
+                for (long long o = beg; o < end; o += 32768) {
+                    const long long nbytes = end - o < 32768 ? end - o : 32768;
+                    l2_prefetch(reinterpret_cast<const uint8_t*>(a.pf_ptr) + o, (uint32_t)(nbytes & ~15ll));
+                }
+            }
             const int pre = nj < 2 ? nj : 2;
             bool issued[2] = {false, false};
             for (int j = 0; j < pre; ++j)
