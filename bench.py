@@ -246,7 +246,7 @@ def run_ours(args, rank, world, local_rank):
     noise = torch.from_numpy(alpa.host_noise(C2["seed"], C2["stride"], n, lane0)).to(dev)
     acts = torch.empty((n, 64, 2), dtype=torch.float32, device=dev)
     traj = torch.empty((n, 64, 3), dtype=torch.float32, device=dev)
-    gathered = [torch.empty_like(acts) for _ in range(world)] if world > 1 else None
+    from paper_2605_08975_b200 import dist as pdist
 
     def step(scene: int):
         if dist is not None:
@@ -254,10 +254,10 @@ def run_ours(args, rank, world, local_rank):
             if rank == 0:
                 gen.synthesize_prefix(prefix.data_ptr(), C2["prefix_seed"] + 1000 * scene,
                                       C2["r"])
-            dist.broadcast(prefix, 0)
+            pdist.broadcast_prefix(prefix, 0)
         gen.generate_device(req, noise.data_ptr(), acts.data_ptr(), traj.data_ptr())
         if dist is not None:
-            dist.all_gather(gathered, acts)
+            pdist.gather_lanes(acts, world * n)
 
     for i in range(args.warmup):
         step(i)

@@ -1,0 +1,269 @@
+// alpa_minivla_shim.hpp -- header-only C++ re-exposure of the reference's
+// action-generation API (minivla, /root/reference/proj) over the C-ABI in
+// alpa_action.h.  A reference caller swaps
+//
+//     minivla::Engine::run_action_generation      pipeline.hpp:145-148
+//     minivla::actions_to_trajectory              pipeline.hpp:90
+//     minivla::initial_speed_from_history         pipeline.hpp:93
+//
+// for the same-named members below; argument meaning and the exception types
+// (ConfigError / IoError / InternalError, common.hpp:12-23) are unchanged.
+// The reasoning stage is out of scope: ReasoningOutput carries the sealed
+// prefix KV as a host f32 buffer [n_prefix][B][2][r][kv] (what
+// Substrate::read(kv.block_buffer(b)) yields, first r tokens per block) or a
+// device pointer in the context dtype.
+#pragma once
+
+#include <array>
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "alpa_action.h"
+
+namespace alpa_shim {
+
+struct Error : std::runtime_error {
+    using std::runtime_error::runtime_error;
+};
+struct IoError : Error {
+    using Error::Error;
+};
+struct ConfigError : Error {
+    using Error::Error;
+};
+struct InternalError : Error {
+    using Error::Error;
+};
+
+inline void check(int rc, const alpa_ctx* ctx) {
+    if (rc == ALPA_OK) return;
+    const std::string msg = alpa_last_error(ctx);
+    if (rc == ALPA_ERR_IO) throw IoError(msg);
+    if (rc == ALPA_ERR_CONFIG) throw ConfigError(msg);
+    throw InternalError(msg);
+}
+
+enum class Topology { Multi, Single };           // pipeline.hpp:48
+enum class KvStrategy { Dynamic, Static };       // kv_cache.hpp:9
+enum class ExecMode { Eager, Graph };            // model.hpp:43
+enum class Dtype { F32 = ALPA_DTYPE_F32, BF16 = ALPA_DTYPE_BF16 };
+
+// ModelConfig (model.hpp:12-29) + compute dtype.
+struct ModelConfig {
+    std::int64_t vision_blocks = 4;
+    std::int64_t decoder_blocks = 6;
+    std::int64_t hidden_dim = 64;
+    std::int64_t action_hidden_dim = 32;
+    std::int64_t kv_dim = 32;
+    std::int64_t heads = 4;
+    std::int64_t vocab_size = 512;
+    std::int64_t patch_size = 14;
+    std::int64_t action_steps = 64;
+    std::int64_t diffusion_iters = 10;
+    float update_scale = 0.1f;
+    std::int64_t max_new_tokens = 256;
+    std::uint64_t weight_seed = 1234;
+    Dtype dtype = Dtype::F32;
+
+    alpa_model_cfg c() const {
+        alpa_model_cfg m{};
+        m.vision_blocks = vision_blocks;
+        m.decoder_blocks = decoder_blocks;
+        m.hidden_dim = hidden_dim;
+        m.action_hidden_dim = action_hidden_dim;
+        m.kv_dim = kv_dim;
+        m.heads = heads;
+        m.vocab_size = vocab_size;
+        m.patch_size = patch_size;
+        m.action_steps = action_steps;
+        m.diffusion_iters = diffusion_iters;
+        m.update_scale = update_scale;
+        m.dtype = static_cast<int32_t>(dtype);
+        m.weight_seed = weight_seed;
+        return m;
+    }
+    void validate() const {  // ModelConfig::validate, model.cpp:9-24
+        const alpa_model_cfg m = c();
+        check(alpa_validate_cfg(&m), nullptr);
+    }
+};
+
+struct ActionStep {  // model.hpp:31-34
+    float accel = 0.0f;
+    float curvature = 0.0f;
+};
+struct ActionSequence {  // model.hpp:38-40
+    std::vector<ActionStep> steps;
+};
+struct Pose {  // pipeline.hpp:18-22
+    float x = 0.0f, y = 0.0f, yaw = 0.0f;
+};
+struct PoseHistory {
+    std::array<Pose, 16> poses{};
+};
+struct Trajectory {
+    std::vector<Pose> poses;
+};
+
+// The InferenceRequest fields the path consumes (pipeline.hpp:97-113).
+struct InferenceRequest {
+    PoseHistory pose_history;
+    std::int64_t num_trajectories = 1;
+    Topology topology = Topology::Multi;
+    KvStrategy kv_strategy = KvStrategy::Dynamic;
+    ExecMode executor = ExecMode::Eager;
+    std::uint64_t action_init_seed = 2;
+    std::uint64_t action_seed_stride = 1;
+};
+
+// Sealed reasoning prefix (the part of ReasoningOutput the path reads,
+// pipeline.hpp:120-126).
+struct ReasoningOutput {
+    std::vector<float> kv_host;   // [n_prefix][B][2][r][kv] f32, or empty
+    const void* kv_device = nullptr;  // same shape, context dtype, or null
+    std::int64_t n_prefix = 1;
+    std::int64_t reasoning_len = 0;   // r
+    std::uint64_t version = 0;        // bump when the content changes
+};
+
+// Model::DiffusionResult (model.hpp:155-160), counters redefined: one graph
+// launch per call, kernel nodes instead of substrate commands.
+struct DiffusionResult {
+    std::vector<double> iter_ms;
+    std::int64_t graph_commands = 0;
+    std::int64_t graph_launches = 0;
+    double device_ms = 0.0;
+};
+
+inline float initial_speed_from_history(const PoseHistory& h) {  // pipeline.cpp:150-156
+    float buf[16 * 3];
+    for (int i = 0; i < 16; ++i) {
+        buf[i * 3] = h.poses[i].x;
+        buf[i * 3 + 1] = h.poses[i].y;
+        buf[i * 3 + 2] = h.poses[i].yaw;
+    }
+    return alpa_initial_speed(buf);
+}
+
+// The action-generation half of minivla::Engine on one GPU context.
+class Engine {
+public:
+    explicit Engine(const ModelConfig& cfg, int device = 0) : cfg_(cfg) {
+        const alpa_model_cfg m = cfg.c();
+        check(alpa_ctx_create(&m, device, &ctx_), nullptr);
+        check(alpa_load_weights_seeded(ctx_, cfg.weight_seed, -1), ctx_);
+    }
+    ~Engine() { alpa_ctx_destroy(ctx_); }
+    Engine(const Engine&) = delete;
+    Engine& operator=(const Engine&) = delete;
+
+    const ModelConfig& config() const { return cfg_; }
+    alpa_ctx* handle() { return ctx_; }
+
+    // Engine::run_action_generation (pipeline.cpp:399-436): no prefix
+    // replication (every lane attends the single prefix copy in place).
+    std::vector<ActionSequence> run_action_generation(ReasoningOutput& reasoning,
+                                                      const InferenceRequest& request,
+                                                      DiffusionResult* diff = nullptr,
+                                                      std::int64_t* kv_bytes = nullptr) {
+        bind(reasoning);
+        const std::int64_t n = request.num_trajectories;
+        const std::int64_t A = cfg_.action_steps;
+        alpa_request r = to_c(request);
+        std::vector<float> acts(static_cast<size_t>(n > 0 ? n : 0) * A * 2);
+        alpa_stats st{};
+        check(alpa_generate(ctx_, &r, acts.data(), nullptr, &st), ctx_);
+        if (kv_bytes) *kv_bytes = st.kv_bytes;
+        if (diff) {
+            diff->iter_ms.assign(static_cast<size_t>(cfg_.diffusion_iters),
+                                 st.device_ms / static_cast<double>(cfg_.diffusion_iters));
+            diff->graph_commands = st.graph_nodes;
+            diff->graph_launches = st.graph_launches;
+            diff->device_ms = st.device_ms;
+        }
+        std::vector<ActionSequence> out(static_cast<size_t>(n));
+        for (std::int64_t l = 0; l < n; ++l) {
+            out[l].steps.resize(static_cast<size_t>(A));
+            for (std::int64_t i = 0; i < A; ++i)
+                out[l].steps[i] = {acts[(l * A + i) * 2], acts[(l * A + i) * 2 + 1]};
+        }
+        return out;
+    }
+
+    // run_action_generation + the postprocessing rollout in one device pass
+    // (Engine::infer's action-gen + postprocessing, pipeline.cpp:462-479).
+    std::vector<Trajectory> generate_trajectories(ReasoningOutput& reasoning,
+                                                  const InferenceRequest& request,
+                                                  std::vector<ActionSequence>* actions = nullptr) {
+        bind(reasoning);
+        const std::int64_t n = request.num_trajectories;
+        const std::int64_t A = cfg_.action_steps;
+        alpa_request r = to_c(request);
+        std::vector<float> acts(static_cast<size_t>(n > 0 ? n : 0) * A * 2);
+        std::vector<float> traj(static_cast<size_t>(n > 0 ? n : 0) * A * 3);
+        check(alpa_generate(ctx_, &r, acts.data(), traj.data(), nullptr), ctx_);
+        std::vector<Trajectory> out(static_cast<size_t>(n));
+        if (actions) actions->assign(static_cast<size_t>(n), ActionSequence{});
+        for (std::int64_t l = 0; l < n; ++l) {
+            out[l].poses.resize(static_cast<size_t>(A));
+            for (std::int64_t i = 0; i < A; ++i) {
+                const float* p = &traj[(l * A + i) * 3];
+                out[l].poses[i] = {p[0], p[1], p[2]};
+            }
+            if (actions) {
+                (*actions)[l].steps.resize(static_cast<size_t>(A));
+                for (std::int64_t i = 0; i < A; ++i)
+                    (*actions)[l].steps[i] = {acts[(l * A + i) * 2], acts[(l * A + i) * 2 + 1]};
+            }
+        }
+        return out;
+    }
+
+    // actions_to_trajectory (pipeline.cpp:124-148) on the device, bit-exact.
+    Trajectory actions_to_trajectory(const ActionSequence& a, float initial_speed) {
+        const std::int64_t A = static_cast<std::int64_t>(a.steps.size());
+        std::vector<float> in(static_cast<size_t>(A) * 2), out(static_cast<size_t>(A) * 3);
+        for (std::int64_t i = 0; i < A; ++i) {
+            in[i * 2] = a.steps[i].accel;
+            in[i * 2 + 1] = a.steps[i].curvature;
+        }
+        check(alpa_rollout(ctx_, in.data(), 1, initial_speed, out.data()), ctx_);
+        Trajectory t;
+        t.poses.resize(static_cast<size_t>(A));
+        for (std::int64_t i = 0; i < A; ++i) t.poses[i] = {out[i * 3], out[i * 3 + 1], out[i * 3 + 2]};
+        return t;
+    }
+
+private:
+    void bind(const ReasoningOutput& r) {
+        if (bound_version_ == r.version && bound_ptr_ == &r) return;
+        if (r.kv_device)
+            check(alpa_bind_prefix_device(ctx_, r.kv_device, r.n_prefix, r.reasoning_len), ctx_);
+        else
+            check(alpa_bind_prefix(ctx_, r.kv_host.data(), r.n_prefix, r.reasoning_len), ctx_);
+        bound_version_ = r.version;
+        bound_ptr_ = &r;
+    }
+    static alpa_request to_c(const InferenceRequest& q) {
+        alpa_request r{};
+        r.num_trajectories = q.num_trajectories;
+        r.lane0 = 0;
+        r.action_init_seed = q.action_init_seed;
+        r.action_seed_stride = q.action_seed_stride;
+        r.diffusion_iters = 0;
+        r.topology = q.topology == Topology::Single ? ALPA_TOPOLOGY_SINGLE : ALPA_TOPOLOGY_MULTI;
+        r.kv_strategy = q.kv_strategy == KvStrategy::Static ? ALPA_KV_STATIC : ALPA_KV_DYNAMIC;
+        r.executor = q.executor == ExecMode::Graph ? ALPA_EXEC_GRAPH : ALPA_EXEC_EAGER;
+        r.v0 = initial_speed_from_history(q.pose_history);
+        return r;
+    }
+
+    ModelConfig cfg_;
+    alpa_ctx* ctx_ = nullptr;
+    std::uint64_t bound_version_ = ~0ull;
+    const ReasoningOutput* bound_ptr_ = nullptr;
+};
+
+}  // namespace alpa_shim

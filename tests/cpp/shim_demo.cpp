@@ -1,0 +1,57 @@
+// Reference-style caller of the C++ shim (include/alpa_minivla_shim.hpp): the
+// code a minivla user writes around Engine::run_action_generation, unchanged
+// except for the namespace.  Used by tests/test_shim.py.
+//
+//   shim_demo <prefix.bin> <r> <n> <out_actions.bin> <out_traj.bin>
+// exit codes follow the reference CLI (cli.cpp:528-540): 1 io, 2 config, 3 internal.
+#include <cstdio>
+#include <fstream>
+#include <vector>
+
+#include "alpa_minivla_shim.hpp"
+
+using namespace alpa_shim;
+
+int main(int argc, char** argv) {
+    if (argc != 6) return 1;
+    try {
+        ModelConfig cfg;  // fixtures/default_config.json model block
+        Engine engine(cfg);
+        ReasoningOutput reasoning;
+        reasoning.reasoning_len = std::atoll(argv[2]);
+        const size_t n_kv = static_cast<size_t>(cfg.decoder_blocks) * 2 * reasoning.reasoning_len * cfg.kv_dim;
+        reasoning.kv_host.resize(n_kv);
+        std::ifstream in(argv[1], std::ios::binary);
+        if (!in.read(reinterpret_cast<char*>(reasoning.kv_host.data()), n_kv * sizeof(float)))
+            throw IoError("cannot read prefix");
+        InferenceRequest req;
+        req.num_trajectories = std::atoll(argv[3]);
+        req.topology = Topology::Single;
+        req.kv_strategy = KvStrategy::Static;
+        req.executor = ExecMode::Graph;
+        for (int j = 0; j < 16; ++j) req.pose_history.poses[j] = {-(15.0f - j) * 5.0f * 0.1f, 0.f, 0.f};
+        DiffusionResult diff;
+        std::int64_t kv_bytes = 0;
+        const auto actions = engine.run_action_generation(reasoning, req, &diff, &kv_bytes);
+        const float v0 = initial_speed_from_history(req.pose_history);
+        std::ofstream oa(argv[4], std::ios::binary), ot(argv[5], std::ios::binary);
+        for (const auto& a : actions) {
+            oa.write(reinterpret_cast<const char*>(a.steps.data()), a.steps.size() * sizeof(ActionStep));
+            const Trajectory t = engine.actions_to_trajectory(a, v0);
+            ot.write(reinterpret_cast<const char*>(t.poses.data()), t.poses.size() * sizeof(Pose));
+        }
+        std::printf("ok graph_commands=%lld kv_bytes=%lld device_ms=%.3f\n",
+                    static_cast<long long>(diff.graph_commands), static_cast<long long>(kv_bytes),
+                    diff.device_ms);
+        return 0;
+    } catch (const IoError& e) {
+        std::fprintf(stderr, "io error: %s\n", e.what());
+        return 1;
+    } catch (const ConfigError& e) {
+        std::fprintf(stderr, "config error: %s\n", e.what());
+        return 2;
+    } catch (const InternalError& e) {
+        std::fprintf(stderr, "internal error: %s\n", e.what());
+        return 3;
+    }
+}

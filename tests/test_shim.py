@@ -1,0 +1,51 @@
+"""The C++ drop-in: a reference-style caller compiled against
+include/alpa_minivla_shim.hpp and linked to libalpa_action.so.
+
+CPU: it compiles and links (no compute).  GPU: it reproduces the golden
+config-1 actions / trajectories and maps errors to the reference exit codes.
+"""
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PKG = os.path.join(ROOT, "paper_2605_08975_b200")
+
+
+def build_demo(tmp_path):
+    exe = str(tmp_path / "shim_demo")
+    subprocess.run(["g++", "-std=c++17", "-O2", "-I", os.path.join(ROOT, "include"),
+                    os.path.join(ROOT, "tests", "cpp", "shim_demo.cpp"), "-L", PKG,
+                    "-lalpa_action", f"-Wl,-rpath,{PKG}", "-o", exe], check=True)
+    return exe
+
+
+def test_shim_compiles_and_links(tmp_path):
+    exe = build_demo(tmp_path)
+    assert os.path.exists(exe)
+
+
+@pytest.mark.gpu
+def test_shim_reproduces_golden(tmp_path, golden):
+    exe = build_demo(tmp_path)
+    pre = tmp_path / "prefix.bin"
+    golden["prefix"].astype(np.float32).tofile(pre)
+    oa, ot = tmp_path / "a.bin", tmp_path / "t.bin"
+    r = golden["prefix"].shape[2]
+    out = subprocess.run([exe, str(pre), str(r), "6", str(oa), str(ot)], capture_output=True,
+                         text=True)
+    assert out.returncode == 0, out.stderr
+    acts = np.fromfile(oa, np.float32).reshape(6, 64, 2)
+    traj = np.fromfile(ot, np.float32).reshape(6, 64, 3)
+    ea, et = golden["expected"]["n6_k10_actions"], golden["expected"]["n6_k10_traj"]
+    assert np.linalg.norm(acts - ea) / np.linalg.norm(ea) <= 1e-4
+    assert np.linalg.norm(traj - et) / np.linalg.norm(et) <= 1e-4
+    # N = 0 -> ConfigError -> exit code 2 (pipeline.cpp:203-205, cli.cpp:528-540)
+    bad = subprocess.run([exe, str(pre), str(r), "0", str(oa), str(ot)], capture_output=True)
+    assert bad.returncode == 2
+    # missing prefix file -> IoError -> exit code 1
+    bad = subprocess.run([exe, str(tmp_path / "nope.bin"), str(r), "6", str(oa), str(ot)],
+                         capture_output=True)
+    assert bad.returncode == 1
