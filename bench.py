@@ -302,11 +302,15 @@ def run_ours(args, rank, world, local_rank):
            "d2h_bytes_per_step": int(st["d2h_bytes"]) + 4}
 
     # per-kernel breakdown (CUDA events around each launch of one eager scene)
-    prof = gen.profile(req, iters=K)
+    allprof = gen.profile(req, iters=K)
+    # "span:<op>" entries are per-op spans inside the persistent iteration
+    # kernel (globaltimer stamps), not separate launches
+    prof = [p for p in allprof if not p["name"].startswith("span:")]
+    spans = [p for p in allprof if p["name"].startswith("span:")]
     pk = peaks()
     total_ms = sum(p["total_ms"] for p in prof)
     dom = max(prof, key=lambda p: p["total_ms"])
-    tensor_kernels = ("gemm", "attention")
+    tensor_kernels = ("gemm", "attention", "iteration")
     bound = "tensor" if dom["name"].startswith(tensor_kernels) else "hbm"
     if bound == "tensor":
         ach = dom["flops"] / (dom["total_ms"] * 1e-3) / 1e12
@@ -344,6 +348,9 @@ def run_ours(args, rank, world, local_rank):
                                 "tflops": p["flops"] / max(p["total_ms"], 1e-9) / 1e9,
                                 "gbs": p["bytes"] / max(p["total_ms"], 1e-9) / 1e6}
                     for p in prof},
+        "op_spans": {p["name"][5:]: {"ms_per_scene": p["total_ms"], "count": p["launches"],
+                                      "tflops": p["flops"] / max(p["total_ms"], 1e-9) / 1e9}
+                     for p in spans},
         "gpu_launches": gpu_launches,
         "clocks": clk.summary(),
     }

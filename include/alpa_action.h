@@ -165,6 +165,14 @@ typedef struct alpa_kernel_prof {
 } alpa_kernel_prof;
 int alpa_profile(alpa_ctx* ctx, const alpa_request* req, int64_t iters, alpa_kernel_prof* out,
                  int32_t max_out, int32_t* n_out);
+/* Diagnostics: per-CTA event times [n_ops][grid][16] (globaltimer ns) of the
+ * last profiled persistent-kernel iteration; needs ALPA_MK_TRACE=1 in the
+ * environment when the plan was built.  Events: 0 inputs ready (producer),
+ * 1 first stage landed (MMA), 2 last MMA issued, 3 accumulator ready
+ * (epilogue), 4 split rendezvous, 5 item published, 6 weight stages issued,
+ * 7 accumulator drained, 8 fixup done, 9 publish fences passed. */
+int alpa_debug_mk_trace(alpa_ctx* ctx, unsigned long long* out, int64_t max_elems,
+                        int64_t* n_ops, int64_t* grid);
 
 /* ---- host helpers (bit-exact restatements of the reference host code) -- */
 /* Rng::normal noise for lanes [lane0, lane0+n): out [n][steps][2]. */

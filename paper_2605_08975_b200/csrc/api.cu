@@ -138,6 +138,7 @@ void run_loop(Ctx& c, const alpa_request& r, int64_t K, alpa_stats* st) {
     cudaStream_t s = c.stream;
     const float v0 = r.v0;
     ALPA_CUDA(cudaMemcpyAsync(c.d_scalars, &v0, sizeof(float), cudaMemcpyHostToDevice, s));
+    alpa::prepare_iteration(c, n);
     if (r.executor == ALPA_EXEC_GRAPH) {
         if (!c.graph.exec || c.graph.n != n || c.graph.k != K) {
             alpa::invalidate_graph(c);
@@ -486,7 +487,9 @@ int alpa_profile(alpa_ctx* h, const alpa_request* req, int64_t iters, alpa_kerne
         const float v0 = r.v0;
         ALPA_CUDA(cudaMemcpyAsync(c->d_scalars, &v0, sizeof(float), cudaMemcpyHostToDevice,
                                   c->stream));
+        alpa::prepare_iteration(*c, n);
         c->prof.clear();
+        c->prof_spans.clear();
         c->ev_next = 0;
         c->prof_on = true;
         try {
@@ -515,13 +518,43 @@ int alpa_profile(alpa_ctx* h, const alpa_request* req, int64_t iters, alpa_kerne
             slot->flops += rec.flops;
             slot->bytes += rec.bytes;
         }
+        for (const auto& sp : c->prof_spans) {
+            // per-op spans inside the persistent launch, reported as "span:<op>"
+            char name[sizeof(agg[0].name)] = {0};
+            std::snprintf(name, sizeof(name), "span:%s", sp.tag);
+            alpa_kernel_prof* slot = nullptr;
+            for (auto& a : agg)
+                if (std::strncmp(a.name, name, sizeof(a.name)) == 0) slot = &a;
+            if (!slot) {
+                agg.push_back(alpa_kernel_prof{});
+                slot = &agg.back();
+                std::strncpy(slot->name, name, sizeof(slot->name) - 1);
+            }
+            slot->launches += 1;
+            slot->total_ms += sp.ms;
+            slot->flops += sp.flops;
+        }
         c->prof.clear();
+        c->prof_spans.clear();
         const int32_t k = (int32_t)std::min<size_t>(agg.size(), (size_t)max_out);
         for (int32_t i = 0; i < k; ++i) out[i] = agg[i];
         *n_out = k;
     });
 }
 
+
+int alpa_debug_mk_trace(alpa_ctx* h, unsigned long long* out, int64_t max_elems, int64_t* n_ops,
+                        int64_t* grid) {
+    Ctx* c = reinterpret_cast<Ctx*>(h);
+    return guarded(c, [&] {
+        if (!c || !out || !n_ops || !grid) fail(ALPA_ERR_CONFIG, "null argument");
+        if (!c->mk.d_trace) fail(ALPA_ERR_INTERNAL, "no persistent-kernel trace (ALPA_MK_TRACE=1 + alpa_profile)");
+        const size_t n = std::min<size_t>(c->mk.trace_elems, (size_t)max_elems);
+        ALPA_CUDA(cudaMemcpy(out, c->mk.d_trace, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+        *n_ops = c->mk.n_ops;
+        *grid = c->mk.grid;
+    });
+}
 
 void alpa_host_noise(uint64_t seed, uint64_t stride, int64_t lane0, int64_t n, int64_t steps,
                      float* out) {

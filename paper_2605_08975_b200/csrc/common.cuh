@@ -50,6 +50,23 @@ __device__ inline float gelu_fast(float x) {
     return __fdividef(x, 1.0f + ex2f(-2.8853900817779268f * z));
 }
 
+// Same erf fit, as 0.5 x (1 + tanh(z)) with the single-MUFU tanh.approx
+// (|err| <= 5e-4 * |x|, below the bf16 quantum of the GELU output).  The
+// persistent kernel's epilogue is MUFU-bound with the ex2 + rcp form.
+__device__ inline float tanh_approx(float x) {
+    float y;
+    asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ inline float gelu_tanh(float x) {
+    const float u = fminf(fmaxf(x * 0.70710678118654752f, -4.5f), 4.5f);
+    const float u2 = u * u;
+    const float z = u * fmaf(fmaf(fmaf(-1.52990796e-04f, u2, -1.10976167e-03f), u2, 1.03380981e-01f), u2,
+                             1.12828571e+00f);
+    const float hx = 0.5f * x;
+    return fmaf(hx, tanh_approx(z), hx);
+}
+
 __device__ inline float warp_sum(float v) {
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
@@ -119,6 +136,11 @@ __device__ inline uint64_t policy_evict_first() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+__device__ inline uint64_t policy_evict_normal() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
 __device__ inline uint64_t policy_evict_last() {
     uint64_t p;
     asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
@@ -162,6 +184,13 @@ __device__ inline void tc_commit(uint64_t* bar) {
             smem_u32(bar))
         : "memory");
 }
+// 32 lanes x 32-bit, 8 consecutive columns per thread.
+__device__ inline void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                   "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+}
 // 32 lanes x 32-bit, 16 consecutive columns per thread.
 __device__ inline void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
     asm volatile(
@@ -194,6 +223,15 @@ __device__ inline void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
         "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]), "r"(r[19]), "r"(r[20]), "r"(r[21]),
         "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]),
         "r"(r[29]), "r"(r[30]), "r"(r[31])
+        : "memory");
+}
+__device__ inline void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+        "%13,%14,%15,%16};" ::"r"(taddr),
+        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]),
+        "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]),
+        "r"(r[15])
         : "memory");
 }
 __device__ inline void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
@@ -279,6 +317,14 @@ __device__ inline void l2_prefetch(const void* p, uint32_t bytes) {
                  : "memory");
 }
 
+// Same with an L2 cache policy (evict_first for once-per-iteration streams).
+__device__ inline void l2_prefetch_hint(const void* p, uint32_t bytes, uint64_t policy) {
+    asm volatile("cp.async.bulk.prefetch.L2.global.L2::cache_hint [%0], %1, %2;" ::"l"(
+                     reinterpret_cast<uint64_t>(p)),
+                 "r"(bytes), "l"(policy)
+                 : "memory");
+}
+
 // TMA bulk copy: local smem -> smem of another CTA of the cluster, completing
 // (complete_tx) on the destination CTA's mbarrier.
 __device__ inline void bulk_copy_to_cluster(uint32_t dst_cluster_addr, uint32_t src_cta_addr,
@@ -288,6 +334,16 @@ __device__ inline void bulk_copy_to_cluster(uint32_t dst_cluster_addr, uint32_t 
         ::"r"(dst_cluster_addr), "r"(src_cta_addr), "r"(bytes), "r"(bar_cluster_addr)
         : "memory");
 }
+
+// TMA tensor store smem -> global (bulk group) and its completion wait.
+__device__ inline void tma_store_2d(const CUtensorMap* m, const void* src, int c0, int c1) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(m)),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1)
+                 : "memory");
+}
+__device__ inline void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ inline void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 // Programmatic dependent launch.
 __device__ inline void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }

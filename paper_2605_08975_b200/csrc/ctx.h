@@ -73,6 +73,34 @@ struct KInfo {
     double flops, bytes;
 };
 
+// Persistent iteration kernel plan (mk.cu): device op list, tensor maps,
+// completion / split counters and the split-partial workspace.
+struct MkState {
+    bool valid = false;
+    int64_t n = -1, uniform = -2, r = -1, prefix_n = -1;
+    const void* prefix = nullptr;
+    void* d_ops = nullptr;
+    int n_ops = 0;
+    CUtensorMap* d_maps = nullptr;
+    int* d_counters = nullptr;
+    size_t counter_ints = 0;
+    float* ws = nullptr;
+    float2* wsml = nullptr;
+    unsigned long long* d_tstamp = nullptr;
+    unsigned long long* d_trace = nullptr;  // ALPA_MK_TRACE=1: [n_ops][G][8] event times
+    size_t trace_elems = 0;
+    std::vector<const char*> tags;
+    std::vector<double> flops;
+    void* fn = nullptr;
+    int smem = 0, grid = 0;
+};
+
+// Per-op span inside a persistent launch (alpa_profile).
+struct ProfSpan {
+    const char* tag;
+    double ms, flops;
+};
+
 struct GraphCache {
     cudaGraphExec_t exec = nullptr;
     int64_t n = -1, k = -1, prefix_id = -2;
@@ -101,6 +129,8 @@ struct Ctx {
     bool tm_pre_valid = false;
 
     Workspace ws;
+    MkState mk;
+    std::vector<ProfSpan> prof_spans;
     GraphCache graph;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     float* d_scalars = nullptr;  // [0] = v0 (rollout), [1] = non-finite flag (int)
@@ -141,6 +171,15 @@ void enqueue_iteration(Ctx& c, int64_t n, cudaStream_t s);  // one diffusion ite
 void enqueue_rollout(Ctx& c, int64_t n, const float* d_actions, float* d_traj, cudaStream_t s);
 void invalidate_graph(Ctx& c);
 void refresh_prefix_map(Ctx& c);  // TMA map of the bound prefix (bf16)
+
+// mk.cu: persistent iteration kernel (bf16 path, uniform prefix)
+bool mk_usable(const Ctx& c);
+void mk_prepare(Ctx& c, int64_t n);
+void mk_release(Ctx& c);
+void mk_enqueue(Ctx& c, int64_t n, cudaStream_t s, unsigned long long* tstamp,
+                unsigned long long* trace = nullptr);
+// Host-side preparation that must happen outside stream capture.
+void prepare_iteration(Ctx& c, int64_t n);
 
 // tma.cu
 void make_tmap_bf16_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,

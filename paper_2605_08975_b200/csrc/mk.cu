@@ -1,0 +1,321 @@
+// Host side of the persistent iteration kernel (mk.cuh): builds the per-scene
+// op plan (device Op[] + tensor maps + counters + split workspace) and
+// launches one cooperative kernel per diffusion iteration.
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
+
+#include "ctx.h"
+#include "mk.cuh"
+
+namespace alpa {
+
+namespace {
+
+using mk::Op;
+
+int g_num_sms = 0;
+int num_sms(Ctx& c) {
+    if (!g_num_sms) {
+        cudaDeviceProp prop{};
+        ALPA_CUDA(cudaGetDeviceProperties(&prop, c.device));
+        g_num_sms = prop.multiProcessorCount;
+    }
+    return g_num_sms;
+}
+
+template <int TN, int HD>
+void* kernel_ptr() {
+    return reinterpret_cast<void*>(mk::iter_kernel<TN, HD>);
+}
+template <int TN, int HD>
+int kernel_smem() {
+    return mk::Cfg<TN, HD>::SMEM;
+}
+
+struct KSel {
+    void* fn;
+    int smem;
+};
+KSel select_kernel(int tn, int hd) {
+#define ALPA_MK_CASE(T, D) \
+    if (tn == T && hd == D) return {kernel_ptr<T, D>(), kernel_smem<T, D>()};
+    ALPA_MK_CASE(64, 64) ALPA_MK_CASE(64, 128) ALPA_MK_CASE(128, 64) ALPA_MK_CASE(128, 128)
+    ALPA_MK_CASE(192, 64) ALPA_MK_CASE(192, 128) ALPA_MK_CASE(256, 64) ALPA_MK_CASE(256, 128)
+#undef ALPA_MK_CASE
+    fail(ALPA_ERR_INTERNAL, "persistent kernel: unsupported token tile / head dim");
+}
+
+// Split-K count: one wave (tiles*S <= G, so the splits of a tile are
+// co-resident), TN divisible by S (each split reduces TN/S rows), >= 2 k-blocks
+// per split; maximise the CTAs used, prefer the smaller S on ties.
+int pick_splits(int tiles, int KB, int tn, int G) {
+    if (tiles >= G) return 1;
+    int best = 1, used = tiles;
+    for (int s = 2; s <= 8; ++s) {
+        if (tn % s || tiles * s > G || KB / s < 2) continue;
+        const int kbs = (KB + s - 1) / s;
+        if ((s - 1) * kbs >= KB) continue;  // every split must own >= 1 k-block
+        if (tiles * s > used) {
+            best = s;
+            used = tiles * s;
+        }
+    }
+    return best;
+}
+
+}  // namespace
+
+bool mk_usable(const Ctx& c) {
+    // ALPA_MK=1 selects the persistent kernel, 0 the per-op kernel sequence
+    const char* e = getenv("ALPA_MK");
+    if (!(e && e[0] == '1') || !c.bf16() || c.uniform_prefix < 0 || !c.tm_pre_valid) return false;
+    const int64_t hd = c.kv() / c.cfg.heads;
+    return hd == 64 || hd == 128;
+}
+
+void mk_release(Ctx& c) {
+    MkState& m = c.mk;
+    for (void* p : {(void*)m.d_ops, (void*)m.d_maps, (void*)m.d_counters, (void*)m.ws, (void*)m.wsml,
+                    (void*)m.d_tstamp, (void*)m.d_trace})
+        if (p) c.dfree(p);
+    m = MkState{};
+}
+
+void mk_prepare(Ctx& c, int64_t n) {
+    MkState& m = c.mk;
+    if (m.valid && m.n == n && m.prefix == c.prefix && m.uniform == c.uniform_prefix &&
+        m.r == c.prefix_r && m.prefix_n == c.prefix_n)
+        return;
+    mk_release(c);
+    const int G = num_sms(c);
+    const int64_t A = c.steps(), M = n * A, ah = c.ah(), kv = c.kv(), H = c.cfg.heads, r = c.prefix_r;
+    const int hd = (int)(kv / H);
+    const int tn = c.ws.tn;
+    const int64_t B = c.cfg.decoder_blocks;
+    KSel ks = select_kernel(tn, hd);
+
+    // ---- tensor maps (device copies; TMA reads them from global memory)
+    std::vector<CUtensorMap> maps;
+    auto add_map = [&](const CUtensorMap& t) {
+        maps.push_back(t);
+        return (int)maps.size() - 1;
+    };
+    const int mx = add_map(c.ws.tm_x), mh1 = add_map(c.ws.tm_h1), mctx = add_map(c.ws.tm_ctx);
+    const int mq128 = add_map(c.ws.tm_qkv);
+    CUtensorMap tq{};
+    make_tmap_bf16_2d(&tq, c.ws.qkv, 3 * kv, M, 3 * kv * 2, 64, tn);
+    const int mqkv_tn = add_map(tq);  // QKV output (TMA store)
+    CUtensorMap t64{};
+    make_tmap_bf16_2d(&t64, c.ws.qkv, 3 * kv, M, 3 * kv * 2, 64, 64);
+    const int mq64 = add_map(t64);
+    const uint64_t pre_rows = (uint64_t)c.prefix_n * B * 2 * r;
+    make_tmap_bf16_2d(&t64, c.prefix, (uint64_t)kv, pre_rows, (uint64_t)kv * 2, 64, 64);
+    const int mpre = add_map(t64);
+    const int menc1 = add_map(c.mlp1.tmap), menc2 = add_map(c.mlp2.tmap);
+    std::vector<int> mblk(B * 4);
+    for (int64_t b = 0; b < B; ++b) {
+        mblk[b * 4 + 0] = add_map(c.blocks[b].qkv.tmap);
+        mblk[b * 4 + 1] = add_map(c.blocks[b].o.tmap);
+        mblk[b * 4 + 2] = add_map(c.blocks[b].mlp1.tmap);
+        mblk[b * 4 + 3] = add_map(c.blocks[b].mlp2.tmap);
+    }
+    m.d_maps = (CUtensorMap*)c.dalloc(maps.size() * sizeof(CUtensorMap));
+    ALPA_CUDA(cudaMemcpy(m.d_maps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+    auto dm = [&](int i) { return (const CUtensorMap*)(m.d_maps + i); };
+
+    // ---- ops
+    std::vector<Op> ops;
+    std::vector<const char*> tags;
+    std::vector<double> flops;
+    int split_ctr = 0;
+    size_t ws_floats = 16, wsml_elems = 16;
+    const int tiles_t = (int)((M + tn - 1) / tn);
+    const float2* stats = c.ws.stats;
+    auto wb = [](const Linear& L) { return (long long)(L.in * L.out * 2); };
+    auto push = [&](Op op, const char* tag, double f) {
+        op.dep = ops.empty() ? -1 : (int)ops.size() - 1;
+        op.dep_count = ops.empty() ? 0 : ops.back().n_items;
+        ops.push_back(op);
+        tags.push_back(tag);
+        flops.push_back(f);
+    };
+    // split-K caps per op kind (ALPA_MK_SPLITS="qkv,o,mlp1,mlp2,enc1,enc2"); a
+    // split op pays an fp32 partial round trip through L2, so only the deep-K
+    // MLP2 (K = 4 ah) splits by default
+    int cap[6] = {1, 1, 1, 4, 1, 4};
+    if (const char* e = getenv("ALPA_MK_SPLITS"))
+        std::sscanf(e, "%d,%d,%d,%d,%d,%d", &cap[0], &cap[1], &cap[2], &cap[3], &cap[4], &cap[5]);
+    auto gemm = [&](const Linear& L, int mw, int mxm, int epi, void* out, int64_t ldo, bool produce,
+                    bool consume, const void* pf, long long pfb, const char* tag, int kind) {
+        Op op{};
+        op.kind = mk::OP_GEMM;
+        op.epi = epi;
+        op.nf = (int)L.out;
+        op.k = (int)L.in;
+        op.tiles_f = op.nf / 128;
+        op.tiles_t = tiles_t;
+        const int tiles = op.tiles_f * op.tiles_t, KB = op.k / 64;
+        op.splits = std::min(cap[kind], pick_splits(tiles, KB, tn, G));
+        op.kbs = (KB + op.splits - 1) / op.splits;
+        op.n_items = tiles * op.splits;
+        op.split_base = split_ctr;
+        split_ctr += tiles;
+        op.tmW = dm(mw);
+        op.tmX = dm(mxm);
+        op.tmO = out == c.ws.h1 ? dm(mh1) : out == c.ws.qkv ? dm(mqkv_tn) : nullptr;
+        op.tmXB = dm(mx);
+        op.bias = L.b;
+        op.colsum = consume ? L.colsum : nullptr;
+        op.out = out;
+        op.ldo = ldo;
+        if (produce) {
+            op.stats_out = c.ws.stats;
+            op.xb_out = (__nv_bfloat16*)c.ws.x;
+        }
+        if (consume) op.stats_in = stats;
+        op.pf_ptr = pf;
+        op.pf_bytes = pfb;
+        if (op.splits > 1) ws_floats = std::max(ws_floats, (size_t)op.splits * M * op.nf);
+        push(op, tag, 2.0 * M * L.in * L.out);
+    };
+    const int64_t pre_block = 2 * r * kv * 2;
+    auto prefix_of = [&](int64_t b) {
+        return (const void*)((const uint8_t*)c.prefix + (c.uniform_prefix * B + b) * pre_block);
+    };
+
+    {
+        Op op{};
+        op.kind = mk::OP_ENCODE;
+        op.n_items = (int)((M + 7) / 8);
+        push(op, "encode", 4.0 * M * ah);
+    }
+    gemm(c.mlp1, menc1, mx, EPI_GELU_BF16, c.ws.h1, 4 * ah, false, false, c.mlp2.w, wb(c.mlp2),
+         "gemm_enc_mlp1", 4);
+    gemm(c.mlp2, menc2, mh1, EPI_F32, c.ws.e, ah, true, false, c.blocks[0].qkv.w, wb(c.blocks[0].qkv),
+         "gemm_enc_mlp2", 5);
+    const int qtiles = (int)((M + 127) / 128);
+    const int nbp = (int)((r + 63) / 64);
+    for (int64_t b = 0; b < B; ++b) {
+        const Block& blk = c.blocks[b];
+        gemm(blk.qkv, mblk[b * 4 + 0], mx, EPI_LN_BF16, c.ws.qkv, 3 * kv, false, true, prefix_of(b),
+             pre_block, "gemm_qkv", 0);
+        {
+            Op op{};
+            op.kind = mk::OP_ATTN;
+            op.tiles_f = (int)H;
+            op.tiles_t = qtiles;
+            const int tiles = (int)H * qtiles;
+            const int nbt_min = nbp + 1;
+            op.splits = tiles >= G ? 1 : std::max(1, std::min({G / tiles, nbt_min, 6}));
+            op.n_items = tiles * op.splits;
+            op.split_base = split_ctr;
+            split_ctr += tiles;
+            op.nbp = nbp;
+            op.tmW = dm(mpre);
+            op.tmX = dm(mq64);
+            op.tmQ = dm(mq128);
+            op.out = c.ws.ctxb;
+            const int64_t blkrow = (c.uniform_prefix * B + b) * 2;
+            op.pre_k_row = blkrow * r;
+            op.pre_v_row = (blkrow + 1) * r;
+            op.pf_ptr = blk.o.w;
+            op.pf_bytes = wb(blk.o);
+            ws_floats = std::max(ws_floats, (size_t)2 * op.splits * M * kv);
+            wsml_elems = std::max(wsml_elems, (size_t)2 * op.splits * M * H);
+            push(op, "attention", 4.0 * n * A * (r + A) * kv);
+        }
+        gemm(blk.o, mblk[b * 4 + 1], mctx, EPI_RESID_F32, c.ws.e, ah, true, false, blk.mlp1.w,
+             wb(blk.mlp1), "gemm_o", 1);
+        gemm(blk.mlp1, mblk[b * 4 + 2], mx, EPI_LN_GELU_BF16, c.ws.h1, 4 * ah, false, true, blk.mlp2.w,
+             wb(blk.mlp2), "gemm_mlp1", 2);
+        const bool last = b + 1 == B;
+        gemm(blk.mlp2, mblk[b * 4 + 3], mh1, EPI_RESID_F32, c.ws.e, ah, true, false,
+             last ? nullptr : c.blocks[b + 1].qkv.w, last ? 0 : wb(c.blocks[b + 1].qkv), "gemm_mlp2", 3);
+    }
+    {
+        Op op{};
+        op.kind = mk::OP_HEAD;
+        op.n_items = (int)((M + 7) / 8);
+        push(op, "head_update", 4.0 * M * ah + 8.0 * M);
+    }
+
+    m.n_ops = (int)ops.size();
+    m.d_ops = (Op*)c.dalloc(ops.size() * sizeof(Op));
+    ALPA_CUDA(cudaMemcpy(m.d_ops, ops.data(), ops.size() * sizeof(Op), cudaMemcpyHostToDevice));
+    m.counter_ints = (size_t)m.n_ops + split_ctr;
+    m.d_counters = (int*)c.dalloc(m.counter_ints * sizeof(int));
+    ALPA_CUDA(cudaMemset(m.d_counters, 0, m.counter_ints * sizeof(int)));
+    m.ws = (float*)c.dalloc(ws_floats * sizeof(float));
+    m.wsml = (float2*)c.dalloc(wsml_elems * sizeof(float2));
+    m.d_tstamp = (unsigned long long*)c.dalloc((m.n_ops + 1) * sizeof(unsigned long long));
+    if (const char* e = getenv("ALPA_MK_TRACE"); e && e[0] == '1') {
+        m.trace_elems = (size_t)m.n_ops * G * 16;
+        m.d_trace = (unsigned long long*)c.dalloc(m.trace_elems * sizeof(unsigned long long));
+    }
+    m.tags = tags;
+    m.flops = flops;
+    m.fn = ks.fn;
+    m.smem = ks.smem;
+    m.grid = G;
+    ALPA_CUDA(cudaFuncSetAttribute(ks.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, ks.smem));
+    int occ = 0;
+    ALPA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ks.fn, mk::Cfg<64, 64>::THREADS, ks.smem));
+    if (occ < 1) fail(ALPA_ERR_INTERNAL, "persistent kernel does not fit on an SM");
+    m.n = n;
+    m.prefix = c.prefix;
+    m.uniform = c.uniform_prefix;
+    m.r = r;
+    m.prefix_n = c.prefix_n;
+    m.valid = true;
+}
+
+void mk_enqueue(Ctx& c, int64_t n, cudaStream_t s, unsigned long long* tstamp,
+                unsigned long long* trace) {
+    MkState& m = c.mk;
+    if (!m.valid || m.n != n) fail(ALPA_ERR_INTERNAL, "persistent kernel plan not prepared");
+    mk::Params p{};
+    p.ops = (const Op*)m.d_ops;
+    p.n_ops = m.n_ops;
+    p.done = m.d_counters;
+    p.splitc = m.d_counters + m.n_ops;
+    p.ws = m.ws;
+    p.wsml = m.wsml;
+    p.M = (int)(n * c.steps());
+    p.ah = (int)c.ah();
+    p.kv = (int)c.kv();
+    p.H = (int)c.cfg.heads;
+    p.r = (int)c.prefix_r;
+    p.nft = (int)(c.ah() / 128);
+    p.alpha = 1.0f / sqrtf((float)(c.kv() / c.cfg.heads));
+    p.update_scale = c.cfg.update_scale;
+    p.actions = c.ws.actions;
+    p.w_in = (const float*)c.act_in.w;
+    p.b_in = c.act_in.b;
+    p.pos = c.pos;
+    p.w_head = (const float*)c.head.w;
+    p.b_head = c.head.b;
+    p.e = c.ws.e;
+    p.x = (__nv_bfloat16*)c.ws.x;
+    p.tstamp = tstamp;
+    p.trace = trace;
+    if (const char* e = getenv("ALPA_MK_FLAGS")) p.flags = atoi(e);
+    ALPA_CUDA(cudaMemsetAsync(m.d_counters, 0, m.counter_ints * sizeof(int), s));
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)m.grid);
+    cfg.blockDim = dim3(mk::Cfg<64, 64>::THREADS);
+    cfg.dynamicSmemBytes = (size_t)m.smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    void* args[] = {&p};
+    ALPA_CUDA(cudaLaunchKernelExC(&cfg, m.fn, args));
+    c.last_launches++;
+}
+
+}  // namespace alpa

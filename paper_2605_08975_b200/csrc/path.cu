@@ -558,6 +558,7 @@ void ensure_workspace(Ctx& c, int64_t n) {
     if (c.ws.n == n) return;
     // buffers change -> any captured graph is stale
     invalidate_graph(c);
+    mk_release(c);
     Workspace& w = c.ws;
     for (void* p : {(void*)w.actions, (void*)w.traj, (void*)w.e, w.x, w.qkv, w.ctxb, w.h1,
                     (void*)w.counters, (void*)w.lane_map, (void*)w.stats})
@@ -587,7 +588,45 @@ void ensure_workspace(Ctx& c, int64_t n) {
     }
 }
 
+void prepare_iteration(Ctx& c, int64_t n) {
+    if (mk_usable(c)) mk_prepare(c, n);
+}
+
+// One persistent launch; in profiling mode also the per-op completion spans
+// (globaltimer stamps, synchronous).
+void enqueue_iteration_mk(Ctx& c, int64_t n, cudaStream_t s) {
+    if (!c.prof_on) {
+        mk_enqueue(c, n, s, nullptr);
+        return;
+    }
+    MkState& m = c.mk;
+    ProfRec rec{"iteration", pool_event(c), pool_event(c), 0.0, 0.0};
+    for (double f : m.flops) rec.flops += f;
+    ALPA_CUDA(cudaMemsetAsync(m.d_tstamp, 0, m.n_ops * sizeof(unsigned long long), s));
+    ALPA_CUDA(cudaMemsetAsync(m.d_tstamp + m.n_ops, 0xFF, sizeof(unsigned long long), s));
+    ALPA_CUDA(cudaEventRecord(rec.a, s));
+    if (m.d_trace)
+        ALPA_CUDA(cudaMemsetAsync(m.d_trace, 0, m.trace_elems * sizeof(unsigned long long), s));
+    mk_enqueue(c, n, s, m.d_tstamp, m.d_trace);
+    ALPA_CUDA(cudaEventRecord(rec.b, s));
+    c.prof.push_back(rec);
+    std::vector<unsigned long long> ts(m.n_ops + 1);
+    ALPA_CUDA(cudaMemcpyAsync(ts.data(), m.d_tstamp, ts.size() * sizeof(unsigned long long),
+                              cudaMemcpyDeviceToHost, s));
+    ALPA_CUDA(cudaStreamSynchronize(s));
+    unsigned long long prev = ts[m.n_ops];
+    for (int o = 0; o < m.n_ops; ++o) {
+        const double ms = ts[o] > prev ? (ts[o] - prev) * 1e-6 : 0.0;
+        c.prof_spans.push_back(ProfSpan{m.tags[o], ms, m.flops[o]});
+        if (ts[o] > prev) prev = ts[o];
+    }
+}
+
 void enqueue_iteration(Ctx& c, int64_t n, cudaStream_t s) {
+    if (mk_usable(c)) {
+        enqueue_iteration_mk(c, n, s);
+        return;
+    }
     Workspace& w = c.ws;
     const int64_t A = c.steps(), M = n * A, ah = c.ah(), kv = c.kv(), H = c.cfg.heads;
     const int T = (int)M;
