@@ -54,8 +54,8 @@ KSel select_kernel(int tn, int hd) {
 int pick_splits(int tiles, int KB, int tn, int G) {
     if (tiles >= G) return 1;
     int best = 1, used = tiles;
-    for (int s = 2; s <= 8; ++s) {
-        if (tn % s || tiles * s > G || KB / s < 2) continue;
+    for (int s = 2; s <= 4; ++s) {  // fix_t sums at most 4 split partials
+        if (tn % s || (tn / s) % 16 || tiles * s > G || KB / s < 2) continue;
         const int kbs = (KB + s - 1) / s;
         if ((s - 1) * kbs >= KB) continue;  // every split must own >= 1 k-block
         if (tiles * s > used) {
@@ -69,9 +69,10 @@ int pick_splits(int tiles, int KB, int tn, int G) {
 }  // namespace
 
 bool mk_usable(const Ctx& c) {
-    // ALPA_MK=1 selects the persistent kernel, 0 the per-op kernel sequence
+    // default: the persistent kernel; ALPA_MK=0 selects the per-op kernel
+    // sequence (A/B measurements and cross-checks)
     const char* e = getenv("ALPA_MK");
-    if (!(e && e[0] == '1') || !c.bf16() || c.uniform_prefix < 0 || !c.tm_pre_valid) return false;
+    if ((e && e[0] == '0') || !c.bf16() || c.uniform_prefix < 0 || !c.tm_pre_valid) return false;
     const int64_t hd = c.kv() / c.cfg.heads;
     return hd == 64 || hd == 128;
 }
@@ -103,11 +104,26 @@ void mk_prepare(Ctx& c, int64_t n) {
         maps.push_back(t);
         return (int)maps.size() - 1;
     };
-    const int mx = add_map(c.ws.tm_x), mh1 = add_map(c.ws.tm_h1), mctx = add_map(c.ws.tm_ctx);
     const int mq128 = add_map(c.ws.tm_qkv);
-    CUtensorMap tq{};
-    make_tmap_bf16_2d(&tq, c.ws.qkv, 3 * kv, M, 3 * kv * 2, 64, tn);
-    const int mqkv_tn = add_map(tq);  // QKV output (TMA store)
+    // activation maps (TMA load operand / TMA store target) per token tile
+    std::vector<std::pair<std::pair<const void*, int64_t>, std::pair<int, int>>> act_cache;
+    auto act_map = [&](void* base, int64_t inner, int rows) {
+        for (auto& e : act_cache)
+            if (e.first.first == base && e.first.second == inner && e.second.first == rows) return e.second.second;
+        CUtensorMap t{};
+        make_tmap_bf16_2d(&t, base, inner, M, inner * 2, 64, rows);
+        const int id = add_map(t);
+        act_cache.push_back({{base, inner}, {rows, id}});
+        return id;
+    };
+    // token tile per op kind (qkv, o, mlp1, mlp2, enc1, enc2): the few-tile ops
+    // (QKV: 24 feature tiles, O: 16) use half tiles to spread over more SMs
+    // (a mainloop is bound by the bytes each SM streams)
+    int tno[6] = {tn >= 128 ? tn / 2 : tn, tn >= 128 ? tn / 2 : tn, tn, tn, tn, tn};
+    if (const char* e = getenv("ALPA_MK_TN"))
+        std::sscanf(e, "%d,%d,%d,%d,%d,%d", &tno[0], &tno[1], &tno[2], &tno[3], &tno[4], &tno[5]);
+    for (int& v : tno)
+        if (v <= 0 || v > tn || v % 16 || (v / 2) % 8) v = tn;
     CUtensorMap t64{};
     make_tmap_bf16_2d(&t64, c.ws.qkv, 3 * kv, M, 3 * kv * 2, 64, 64);
     const int mq64 = add_map(t64);
@@ -122,9 +138,8 @@ void mk_prepare(Ctx& c, int64_t n) {
         mblk[b * 4 + 2] = add_map(c.blocks[b].mlp1.tmap);
         mblk[b * 4 + 3] = add_map(c.blocks[b].mlp2.tmap);
     }
-    m.d_maps = (CUtensorMap*)c.dalloc(maps.size() * sizeof(CUtensorMap));
-    ALPA_CUDA(cudaMemcpy(m.d_maps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
-    auto dm = [&](int i) { return (const CUtensorMap*)(m.d_maps + i); };
+    // ops reference maps by index until the device copy exists (fixed up below)
+    auto dm = [&](int i) { return reinterpret_cast<const CUtensorMap*>((uintptr_t)(i + 1)); };
 
     // ---- ops
     std::vector<Op> ops;
@@ -132,7 +147,6 @@ void mk_prepare(Ctx& c, int64_t n) {
     std::vector<double> flops;
     int split_ctr = 0;
     size_t ws_floats = 16, wsml_elems = 16;
-    const int tiles_t = (int)((M + tn - 1) / tn);
     const float2* stats = c.ws.stats;
     auto wb = [](const Linear& L) { return (long long)(L.in * L.out * 2); };
     auto push = [&](Op op, const char* tag, double f) {
@@ -148,25 +162,30 @@ void mk_prepare(Ctx& c, int64_t n) {
     int cap[6] = {1, 1, 1, 4, 1, 4};
     if (const char* e = getenv("ALPA_MK_SPLITS"))
         std::sscanf(e, "%d,%d,%d,%d,%d,%d", &cap[0], &cap[1], &cap[2], &cap[3], &cap[4], &cap[5]);
-    auto gemm = [&](const Linear& L, int mw, int mxm, int epi, void* out, int64_t ldo, bool produce,
+    auto gemm = [&](const Linear& L, int mw, void* xin, int epi, void* out, int64_t ldo, bool produce,
                     bool consume, const void* pf, long long pfb, const char* tag, int kind) {
         Op op{};
+        const int ttn = tno[kind];
+        op.tn = ttn;
         op.kind = mk::OP_GEMM;
         op.epi = epi;
         op.nf = (int)L.out;
         op.k = (int)L.in;
         op.tiles_f = op.nf / 128;
-        op.tiles_t = tiles_t;
+        op.tiles_t = (int)((M + ttn - 1) / ttn);
         const int tiles = op.tiles_f * op.tiles_t, KB = op.k / 64;
-        op.splits = std::min(cap[kind], pick_splits(tiles, KB, tn, G));
+        // split-K only for the fp32 residual producers (their finalisation runs in
+        // the TMEM layout, tokens split evenly in 16-token halves per warp half)
+        const bool splittable = epi == EPI_RESID_F32 || epi == EPI_F32;
+        op.splits = splittable ? std::min(cap[kind], pick_splits(tiles, KB, ttn, G)) : 1;
         op.kbs = (KB + op.splits - 1) / op.splits;
         op.n_items = tiles * op.splits;
         op.split_base = split_ctr;
         split_ctr += tiles;
         op.tmW = dm(mw);
-        op.tmX = dm(mxm);
-        op.tmO = out == c.ws.h1 ? dm(mh1) : out == c.ws.qkv ? dm(mqkv_tn) : nullptr;
-        op.tmXB = dm(mx);
+        op.tmX = dm(act_map(xin, L.in, ttn));
+        op.tmO = (out == c.ws.h1 || out == c.ws.qkv) ? dm(act_map(out, L.out, ttn)) : nullptr;
+        op.tmXB = produce ? dm(act_map(c.ws.x, ah, ttn)) : nullptr;
         op.bias = L.b;
         op.colsum = consume ? L.colsum : nullptr;
         op.out = out;
@@ -192,15 +211,15 @@ void mk_prepare(Ctx& c, int64_t n) {
         op.n_items = (int)((M + 7) / 8);
         push(op, "encode", 4.0 * M * ah);
     }
-    gemm(c.mlp1, menc1, mx, EPI_GELU_BF16, c.ws.h1, 4 * ah, false, false, c.mlp2.w, wb(c.mlp2),
+    gemm(c.mlp1, menc1, c.ws.x, EPI_GELU_BF16, c.ws.h1, 4 * ah, false, false, c.mlp2.w, wb(c.mlp2),
          "gemm_enc_mlp1", 4);
-    gemm(c.mlp2, menc2, mh1, EPI_F32, c.ws.e, ah, true, false, c.blocks[0].qkv.w, wb(c.blocks[0].qkv),
+    gemm(c.mlp2, menc2, c.ws.h1, EPI_F32, c.ws.e, ah, true, false, c.blocks[0].qkv.w, wb(c.blocks[0].qkv),
          "gemm_enc_mlp2", 5);
     const int qtiles = (int)((M + 127) / 128);
     const int nbp = (int)((r + 63) / 64);
     for (int64_t b = 0; b < B; ++b) {
         const Block& blk = c.blocks[b];
-        gemm(blk.qkv, mblk[b * 4 + 0], mx, EPI_LN_BF16, c.ws.qkv, 3 * kv, false, true, prefix_of(b),
+        gemm(blk.qkv, mblk[b * 4 + 0], c.ws.x, EPI_LN_BF16, c.ws.qkv, 3 * kv, false, true, prefix_of(b),
              pre_block, "gemm_qkv", 0);
         {
             Op op{};
@@ -223,16 +242,16 @@ void mk_prepare(Ctx& c, int64_t n) {
             op.pre_v_row = (blkrow + 1) * r;
             op.pf_ptr = blk.o.w;
             op.pf_bytes = wb(blk.o);
-            ws_floats = std::max(ws_floats, (size_t)2 * op.splits * M * kv);
-            wsml_elems = std::max(wsml_elems, (size_t)2 * op.splits * M * H);
+            ws_floats = std::max(ws_floats, (size_t)op.splits * M * kv);
+            wsml_elems = std::max(wsml_elems, (size_t)op.splits * M * H);
             push(op, "attention", 4.0 * n * A * (r + A) * kv);
         }
-        gemm(blk.o, mblk[b * 4 + 1], mctx, EPI_RESID_F32, c.ws.e, ah, true, false, blk.mlp1.w,
+        gemm(blk.o, mblk[b * 4 + 1], c.ws.ctxb, EPI_RESID_F32, c.ws.e, ah, true, false, blk.mlp1.w,
              wb(blk.mlp1), "gemm_o", 1);
-        gemm(blk.mlp1, mblk[b * 4 + 2], mx, EPI_LN_GELU_BF16, c.ws.h1, 4 * ah, false, true, blk.mlp2.w,
+        gemm(blk.mlp1, mblk[b * 4 + 2], c.ws.x, EPI_LN_GELU_BF16, c.ws.h1, 4 * ah, false, true, blk.mlp2.w,
              wb(blk.mlp2), "gemm_mlp1", 2);
         const bool last = b + 1 == B;
-        gemm(blk.mlp2, mblk[b * 4 + 3], mh1, EPI_RESID_F32, c.ws.e, ah, true, false,
+        gemm(blk.mlp2, mblk[b * 4 + 3], c.ws.h1, EPI_RESID_F32, c.ws.e, ah, true, false,
              last ? nullptr : c.blocks[b + 1].qkv.w, last ? 0 : wb(c.blocks[b + 1].qkv), "gemm_mlp2", 3);
     }
     {
@@ -242,6 +261,18 @@ void mk_prepare(Ctx& c, int64_t n) {
         push(op, "head_update", 4.0 * M * ah + 8.0 * M);
     }
 
+    m.d_maps = (CUtensorMap*)c.dalloc(maps.size() * sizeof(CUtensorMap));
+    ALPA_CUDA(cudaMemcpy(m.d_maps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
+    auto fix = [&](const CUtensorMap*& t) {
+        if (t) t = m.d_maps + ((uintptr_t)t - 1);
+    };
+    for (Op& op : ops) {
+        fix(op.tmW);
+        fix(op.tmX);
+        fix(op.tmQ);
+        fix(op.tmO);
+        fix(op.tmXB);
+    }
     m.n_ops = (int)ops.size();
     m.d_ops = (Op*)c.dalloc(ops.size() * sizeof(Op));
     ALPA_CUDA(cudaMemcpy(m.d_ops, ops.data(), ops.size() * sizeof(Op), cudaMemcpyHostToDevice));

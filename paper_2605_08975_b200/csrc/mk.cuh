@@ -53,6 +53,7 @@ struct Op {
     int dep, dep_count;      // op whose completion gates this op's inputs, its item count
     int split_base;          // first per-tile split counter of this op
     int nbp;                 // attention: 64-key prefix blocks
+    int tn;                  // GEMM: token tile of this op (<= the kernel's TN)
     const CUtensorMap* tmW;  // GEMM: W^T [nf][k] box {64,128}; attention: prefix box {64,64}
     const CUtensorMap* tmX;  // GEMM: X [M][k] box {64,TN};     attention: qkv box {64,64}
     const CUtensorMap* tmQ;  // attention: qkv box {64,128}
@@ -279,101 +280,29 @@ __device__ inline uint2 pack_bf16x4(float4 v) {
     return pk;
 }
 
-// Reduce the S split partials of rows [rb, re) of a GEMM tile and apply the
-// op's epilogue.  Warp per row (2 rows per warp in flight), lane = 4
-// consecutive features (128 per tile).  LN consumers read mu/rstd of the rows
-// from smem (mu_s/rs_s indexed by row - rb).
-__device__ inline void gemm_fixup(const Params& p, const Op& op, const GemmItem& g, int rb, int re,
-                                  int ew, int lane, const float* mu_s, const float* rs_s) {
-    const int fq = g.f0 + lane * 4;
-    const int S = op.splits;
-    const float4 b4 = *reinterpret_cast<const float4*>(op.bias + fq);
-    float4 c4 = make_float4(0.f, 0.f, 0.f, 0.f);
-    const bool ln_in = op.epi == EPI_LN_BF16 || op.epi == EPI_LN_GELU_BF16;
-    const bool resid = op.epi == EPI_RESID_F32;
-    const bool f32out = resid || op.epi == EPI_F32;
-    if (ln_in) c4 = *reinterpret_cast<const float4*>(op.colsum + fq);
-    for (int tb = rb + ew; tb < re; tb += 16) {
-        float4 acc[2], ev[2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            const int t = tb + 8 * u;
-            const bool ok = t < re;
-            float4 v[8];
-#pragma unroll
-            for (int s = 0; s < 8; ++s)
-                v[s] = (s < S && ok) ? ldcg4(p.ws + ((int64_t)s * p.M + t) * op.nf + fq)
-                                     : make_float4(0.f, 0.f, 0.f, 0.f);
-            ev[u] = (resid && ok) ? ldcg4(reinterpret_cast<const float*>(op.out) + (int64_t)t * op.ldo + fq)
-                                  : make_float4(0.f, 0.f, 0.f, 0.f);
-            acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll
-            for (int s = 0; s < 8; ++s)
-                if (s < S) {
-                    acc[u].x += v[s].x; acc[u].y += v[s].y; acc[u].z += v[s].z; acc[u].w += v[s].w;
-                }
-        }
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            const int t = tb + 8 * u;
-            if (t >= re) continue;  // warp-uniform
-            float4 v;
-            if (ln_in) {
-                const float mu = mu_s[t - rb], rs = rs_s[t - rb];
-                v = make_float4(rs * (acc[u].x - mu * c4.x) + b4.x, rs * (acc[u].y - mu * c4.y) + b4.y,
-                                rs * (acc[u].z - mu * c4.z) + b4.z, rs * (acc[u].w - mu * c4.w) + b4.w);
-            } else {
-                v = make_float4(acc[u].x + b4.x, acc[u].y + b4.y, acc[u].z + b4.z, acc[u].w + b4.w);
-            }
-            if (f32out) {
-                if (resid) v = make_float4(ev[u].x + v.x, ev[u].y + v.y, ev[u].z + v.z, ev[u].w + v.w);
-                *reinterpret_cast<float4*>(reinterpret_cast<float*>(op.out) + (int64_t)t * op.ldo + fq) = v;
-                if (op.stats_out) {
-                    float ps = v.x + v.y + v.z + v.w;
-                    float pq = v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
-#pragma unroll
-                    for (int k = 16; k > 0; k >>= 1) {
-                        ps += __shfl_xor_sync(0xffffffffu, ps, k);
-                        pq += __shfl_xor_sync(0xffffffffu, pq, k);
-                    }
-                    if (lane == 0) op.stats_out[(int64_t)t * p.nft + g.f0 / 128] = make_float2(ps, pq);
-                    *reinterpret_cast<uint2*>(op.xb_out + (int64_t)t * op.ldo + fq) = pack_bf16x4(v);
-                }
-            } else {
-                if (op.epi == EPI_GELU_BF16 || op.epi == EPI_LN_GELU_BF16) {
-                    v.x = gelu_tanh(v.x); v.y = gelu_tanh(v.y); v.z = gelu_tanh(v.z); v.w = gelu_tanh(v.w);
-                }
-                *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(op.out) + (int64_t)t * op.ldo + fq) =
-                    pack_bf16x4(v);
-            }
-        }
-    }
-}
-
 // Merge the 2S attention partials (S KV splits x 2 key halves) of rows
 // [rb, re) of one (head, query tile): log-sum-exp weights, fixed order.
 template <int HD>
 __device__ inline void attn_fixup(const Params& p, const Op& op, const AttnItem& a, int rb, int re,
                                   int ew, int lane) {
-    const int np = 2 * op.splits;
+    const int np = op.splits;  // one (already half-merged) partial per KV split
     const int d = lane * 4;
     for (int t = rb + ew; t < re; t += 8) {
-        float2 ml[12];
-        float4 v[12];
+        float2 ml[6];
+        float4 v[6];
 #pragma unroll
-        for (int q = 0; q < 12; ++q) {
+        for (int q = 0; q < 6; ++q) {
             ml[q] = q < np ? __ldcg(p.wsml + ((int64_t)q * p.M + t) * p.H + a.h) : make_float2(-INFINITY, 0.f);
             v[q] = (q < np && d < HD) ? ldcg4(p.ws + ((int64_t)q * p.M + t) * p.kv + a.h * HD + d)
                                       : make_float4(0.f, 0.f, 0.f, 0.f);
         }
         float mx = -INFINITY;
 #pragma unroll
-        for (int q = 0; q < 12; ++q) mx = fmaxf(mx, ml[q].x);
+        for (int q = 0; q < 6; ++q) mx = fmaxf(mx, ml[q].x);
         float L = 0.f;
         float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int q = 0; q < 12; ++q) {
-            if (q >= np) continue;
+        for (int q = 0; q < 6; ++q) {
             const float w = ml[q].x == -INFINITY ? 0.f : ex2(ml[q].x - mx);
             L += w * ml[q].y;
             o.x += w * v[q].x; o.y += w * v[q].y; o.z += w * v[q].z; o.w += w * v[q].w;
@@ -502,6 +431,79 @@ __device__ __forceinline__ void drain_t(const DrainArgs& a) {
     }
 }
 
+// Split-K finalisation of one thread's owned tokens (TMEM layout): the own
+// split's partial is read from TMEM, the others' from the L2 workspace, summed
+// in split order 0..S-1 (deterministic), + bias (+ staged residual).
+struct FixArgs {
+    uint32_t tacc, testage;
+    int ncol, c0, S, s_own, nf, q, lane;
+    const float* ws;          // workspace at (split 0, first owned token, feature)
+    long long split_stride;   // floats between splits
+    float bf;
+    float* erow;              // f32 output at the first owned token
+    __nv_bfloat16* xrow;      // bf16 copy or null
+    long long ldo;
+    float2* st_part;
+};
+template <bool RESID>
+__device__ __forceinline__ void fix_t(const FixArgs& a) {
+#pragma unroll 1
+    for (int c = 0; c < a.ncol; c += 8) {
+        float pv[4][8];
+#pragma unroll
+        for (int s2 = 0; s2 < 4; ++s2)
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                pv[s2][j] = (s2 < a.S && s2 != a.s_own) ? __ldcg(a.ws + s2 * a.split_stride + (long long)(c + j) * a.nf) : 0.f;
+        uint32_t r[8], rv[8];
+        tmem_ld8(a.tacc + c, r);
+        if constexpr (RESID) tmem_ld8(a.testage + c, rv);
+        tmem_ld_wait();
+        float v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            float acc = 0.f;
+#pragma unroll
+            for (int s2 = 0; s2 < 4; ++s2)
+                if (s2 < a.S) acc += (s2 == a.s_own) ? __uint_as_float(r[j]) : pv[s2][j];
+            float x = acc + a.bf;
+            if constexpr (RESID) x = __uint_as_float(rv[j]) + x;
+            v[j] = x;
+        }
+        float* d = a.erow + (long long)c * a.ldo;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) stg(d + j * a.ldo, v[j]);
+        if (a.xrow) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) stg(a.xrow + (long long)(c + j) * a.ldo, v[j]);
+        }
+        if (a.st_part) {
+            float a1[8], a2[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) { a1[j] = v[j]; a2[j] = v[j] * v[j]; }
+#pragma unroll
+            for (int rr = 0; rr < 3; ++rr) {
+                const int off = 16 >> rr, half = 4 >> rr;
+                const bool up = (a.lane & off) != 0;
+#pragma unroll
+                for (int i2 = 0; i2 < half; ++i2) {
+                    const float s1 = up ? a1[i2] : a1[i2 + half];
+                    const float s2v = up ? a2[i2] : a2[i2 + half];
+                    const float k1 = up ? a1[i2 + half] : a1[i2];
+                    const float k2 = up ? a2[i2 + half] : a2[i2];
+                    a1[i2] = k1 + __shfl_xor_sync(0xffffffffu, s1, off);
+                    a2[i2] = k2 + __shfl_xor_sync(0xffffffffu, s2v, off);
+                }
+            }
+            a1[0] += __shfl_xor_sync(0xffffffffu, a1[0], 2);
+            a2[0] += __shfl_xor_sync(0xffffffffu, a2[0], 2);
+            a1[0] += __shfl_xor_sync(0xffffffffu, a1[0], 1);
+            a2[0] += __shfl_xor_sync(0xffffffffu, a2[0], 1);
+            if ((a.lane & 3) == 0) a.st_part[a.q * 256 + a.c0 + c + ((a.lane >> 2) & 7)] = make_float2(a1[0], a2[0]);
+        }
+    }
+}
+
 // Mode dispatch (each op kind has its own straight-line instance).
 __device__ inline void drain(const DrainArgs& a, bool ln, bool gelu, bool resid, bool f32, bool part) {
     if (part) drain_t<false, false, false, false, false, true>(a);
@@ -615,7 +617,8 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                     tma_prefetch(op.tmX);
                     bool waited = false;
                     for (int it = blockIdx.x; it < op.n_items; it += gridDim.x) {
-                        const GemmItem g = gemm_item(op, it, TN);
+                        const GemmItem g = gemm_item(op, it, op.tn);
+                        const uint32_t stage_tx = C::W_BYTES + op.tn * 128;
                         // weights do not depend on earlier ops: start them first
                         int pre = g.nkb < C::STAGES ? g.nkb : C::STAGES;
                         if (p.flags & MK_NO_PRELOAD) {
@@ -629,7 +632,7 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                         for (int i = 0; i < pre; ++i) {
                             const uint32_t st = (ks + i) % C::STAGES;
                             uint8_t* sb = slot_acquire(ks + i);
-                            mbar_expect_tx(&full[st], C::W_BYTES + C::X_BYTES);
+                            mbar_expect_tx(&full[st], stage_tx);
                             tma_load_2d_hint(sb, op.tmW, &full[st], (g.kb0 + i) * 64, g.f0, wpol);
                         }
                         trace_ev(p, o, TR_PRE);
@@ -644,7 +647,7 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                             uint8_t* sb = smem + st * C::SLOT;
                             if (i >= pre) {
                                 sb = slot_acquire(ks + i);
-                                mbar_expect_tx(&full[st], C::W_BYTES + C::X_BYTES);
+                                mbar_expect_tx(&full[st], stage_tx);
                                 tma_load_2d_hint(sb, op.tmW, &full[st], (g.kb0 + i) * 64, g.f0, wpol);
                             }
                             tma_load_2d(sb + C::W_BYTES, op.tmX, &full[st], (g.kb0 + i) * 64, g.t0);
@@ -710,9 +713,9 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
             for (int o = 0; o < p.n_ops; ++o) {
                 const Op op = p.ops[o];  // register copy: stores must not force reloads
                 if (op.kind == OP_GEMM) {
-                    constexpr uint32_t idesc = idesc_bf16(128, TN);
+                    const uint32_t idesc = idesc_bf16(128, op.tn);
                     for (int it = blockIdx.x; it < op.n_items; it += gridDim.x) {
-                        const GemmItem g = gemm_item(op, it, TN);
+                        const GemmItem g = gemm_item(op, it, op.tn);
                         if (nmma > 0) mbar_wait(acc_empty, (nmma - 1) & 1);
                         for (int i = 0; i < g.nkb; ++i) {
                             const uint32_t st = (ks + i) % C::STAGES, ph = ((ks + i) / C::STAGES) & 1;
@@ -908,12 +911,19 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                 const bool resid = op.epi == EPI_RESID_F32;
                 const bool f32o = resid || op.epi == EPI_F32;
                 for (int it = blockIdx.x; it < op.n_items; it += gridDim.x) {
-                    const GemmItem g = gemm_item(op, it, TN);
-                    if (!split_path && (ln_in || resid)) {
+                    const int TNo = op.tn;
+                    const GemmItem g = gemm_item(op, it, TNo);
+                    // tokens this CTA finalises: the whole tile, or 1/S of it for a split
+                    const int own_lo = split_path ? (g.s * TNo) / op.splits : 0;
+                    const int own_hi = split_path ? ((g.s + 1) * TNo) / op.splits : TNo;
+                    const int own_h = (own_hi - own_lo) / 2;  // per warp half
+                    const int my_lo = own_lo + hh * own_h;    // this warp half's owned tokens
+                    const int my_n = max(0, min(own_h, p.M - (g.t0 + my_lo)));
+                    if ((!split_path && ln_in) || resid) {
                         // inputs of other CTAs (LN statistics, the residual rows)
                         if (et == 0) wait_count(p.done + op.dep, op.dep_count);
                         epi_bar();
-                        if (ln_in && et < TN) {
+                        if (ln_in && et < TNo) {
                             const int t = g.t0 + et;
                             float mu = 0.f, rs = 0.f;
                             if (t < p.M) ln_stats(p, op.stats_in, t, mu, rs);
@@ -921,24 +931,22 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                             rs_s[et] = rs;
                         }
                         if (resid) {
-                            // stage the residual rows (this thread's feature, its half of
-                            // the tokens) into TMEM columns [256, 256 + TN) while the
+                            // stage the residual rows this thread finalises (its feature,
+                            // its owned tokens) into TMEM columns 256 + token while the
                             // mainloop runs: the drain then never waits on L2
                             const int fe = g.f0 + q * 32 + lane;
-                            const int cbe = hh * (TN / 2);
+                            const float* er = reinterpret_cast<const float*>(op.out) + (int64_t)(g.t0 + my_lo) * op.ldo + fe;
 #pragma unroll 1
-                            for (int c = cbe; c < cbe + TN / 2; c += 32) {
-                                uint32_t v0[16], v1[16];
-                                const bool ok1 = c + 16 < cbe + TN / 2 && g.t0 + c + 16 < p.M;
-                                if (g.t0 + c >= p.M) break;
-                                const float* er = reinterpret_cast<const float*>(op.out) + (int64_t)(g.t0 + c) * op.ldo + fe;
+                            for (int c = 0; c < my_n; c += 16) {
+                                uint32_t v0[8], v1[8];
+                                const bool ok1 = c + 8 < my_n;
 #pragma unroll
-                                for (int j = 0; j < 16; ++j) {
-                                    v0[j] = __float_as_uint(__ldcg(er + j * op.ldo));
-                                    v1[j] = ok1 ? __float_as_uint(__ldcg(er + (16 + j) * op.ldo)) : 0u;
+                                for (int j = 0; j < 8; ++j) {
+                                    v0[j] = __float_as_uint(__ldcg(er + (int64_t)(c + j) * op.ldo));
+                                    v1[j] = ok1 ? __float_as_uint(__ldcg(er + (int64_t)(c + 8 + j) * op.ldo)) : 0u;
                                 }
-                                tmem_st16(tbase + lane_off + 256 + c, v0);
-                                if (ok1) tmem_st16(tbase + lane_off + 256 + c + 16, v1);
+                                tmem_st8(tbase + lane_off + 256 + my_lo + c, v0);
+                                if (ok1) tmem_st8(tbase + lane_off + 256 + my_lo + c + 8, v1);
                             }
                             tmem_st_wait();
                         }
@@ -949,7 +957,7 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                     uint8_t* stg_base = smem + C::OFF_STG;
                     const float bf = split_path ? 0.f : op.bias[f];
                     const float cs = (ln_in && !split_path) ? op.colsum[f] : 0.f;
-                    const int cb = hh * (TN / 2);
+                    const int cb = hh * (TNo / 2);
                     const int64_t ldo = split_path ? op.nf : op.ldo;
                     mbar_wait(acc_full, nmma & 1);
                     if (et == 0) trace_ev(p, o, TR_ACC);
@@ -958,24 +966,45 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                         DrainArgs da;
                         da.tacc = tbase + lane_off + cb;
                         da.testage = resid && !split_path ? tbase + lane_off + 256 + cb : 0xffffffffu;
-                        da.ncol = min(TN / 2, max(0, p.M - (g.t0 + cb)));
+                        da.ncol = min(TNo / 2, max(0, p.M - (g.t0 + cb)));
                         da.c0 = cb;
                         da.fl = fl;
                         da.q = q;
                         da.lane = lane;
-                        da.gelu = gelu && !split_path;
+                        da.gelu = gelu;
                         da.bf = bf;
                         da.cs = cs;
-                        da.mu_s = (ln_in && !split_path) ? mu_s : nullptr;
+                        da.mu_s = ln_in ? mu_s : nullptr;
                         da.rs_s = rs_s;
                         da.ldo = ldo;
-                        da.erow = (f32o && !split_path) ? reinterpret_cast<float*>(op.out) + (int64_t)(g.t0 + cb) * ldo + f : nullptr;
-                        da.stg = split_path ? nullptr : stg_base;
-                        da.stg_panel = TN * 128;
-                        da.st_part = (f32o && !split_path && op.stats_out) ? st_part : nullptr;
-                        da.part = split_path ? p.ws + ((int64_t)g.s * p.M + g.t0 + cb) * ldo + f : nullptr;
+                        da.erow = f32o ? reinterpret_cast<float*>(op.out) + (int64_t)(g.t0 + cb) * ldo + f : nullptr;
+                        da.stg = stg_base;
+                        da.stg_panel = TNo * 128;
+                        da.st_part = (f32o && op.stats_out) ? st_part : nullptr;
+                        da.part = nullptr;
                         da.dbg = 0;
-                        drain(da, ln_in, gelu, resid, f32o, split_path);
+                        if (!split_path) {
+                            drain(da, ln_in, gelu, resid, f32o, false);
+                        } else {
+                            // partials of the tokens other splits finalise: [cb, cb+TNo/2)
+                            // minus [own_lo, own_hi), clipped to M
+                            const int hi = min(cb + TNo / 2, p.M - g.t0);
+                            const int r0a = cb, r0b = min(hi, own_lo);
+                            const int r1a = max(cb, own_hi), r1b = hi;
+                            float* part0 = p.ws + ((int64_t)g.s * p.M + g.t0) * ldo + f;
+                            if (r0b > r0a) {
+                                da.tacc = tbase + lane_off + r0a;
+                                da.ncol = r0b - r0a;
+                                da.part = part0 + (int64_t)r0a * ldo;
+                                drain_t<false, false, false, false, false, true>(da);
+                            }
+                            if (r1b > r1a) {
+                                da.tacc = tbase + lane_off + r1a;
+                                da.ncol = r1b - r1a;
+                                da.part = part0 + (int64_t)r1a * ldo;
+                                drain_t<false, false, false, false, false, true>(da);
+                            }
+                        }
                     }
                     if (et == 0) trace_ev(p, o, TR_LOOP);
                     if (!split_path) {
@@ -986,7 +1015,7 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                         if (et == 0) {
                             const CUtensorMap* tmo = f32o ? op.tmXB : op.tmO;
                             tma_store_2d(tmo, stg_base, g.f0, g.t0);
-                            tma_store_2d(tmo, stg_base + TN * 128, g.f0 + 64, g.t0);
+                            tma_store_2d(tmo, stg_base + TNo * 128, g.f0 + 64, g.t0);
                             bulk_commit();
                         }
                     }
@@ -997,17 +1026,47 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                     ++nmma;
                     if (split_path) {
                         split_meet(p, op, o, p.splitc + op.split_base + g.tile, et);
-                        const int rb = g.t0 + (g.s * TN) / op.splits;
-                        const int re = min(p.M, g.t0 + ((g.s + 1) * TN) / op.splits);
-                        if (ln_in) {
-                            if (et < re - rb) ln_stats(p, op.stats_in, rb + et, mu_s[et], rs_s[et]);
+                        // finalise the owned tokens in the TMEM layout: own partial from
+                        // TMEM + the other splits' partials (fixed split order) + bias
+                        // (+ staged residual) -> e, bf16 copy, row statistics
+                        FixArgs fa;
+                        fa.tacc = tbase + lane_off + my_lo;
+                        fa.testage = tbase + lane_off + 256 + my_lo;
+                        fa.ncol = my_n;
+                        fa.c0 = my_lo;
+                        fa.S = op.splits;
+                        fa.s_own = g.s;
+                        fa.ws = p.ws + (int64_t)(g.t0 + my_lo) * op.nf + f;
+                        fa.split_stride = (int64_t)p.M * op.nf;
+                        fa.nf = op.nf;
+                        fa.bf = op.bias[f];
+                        fa.erow = reinterpret_cast<float*>(op.out) + (int64_t)(g.t0 + my_lo) * op.ldo + f;
+                        fa.xrow = op.xb_out ? op.xb_out + (int64_t)(g.t0 + my_lo) * op.ldo + f : nullptr;
+                        fa.ldo = op.ldo;
+                        fa.st_part = op.stats_out ? st_part : nullptr;
+                        fa.q = q;
+                        fa.lane = lane;
+                        if (resid) fix_t<true>(fa);
+                        else fix_t<false>(fa);
+                        if (op.stats_out) {
                             epi_bar();
+                            const int n_own = min(own_hi, p.M - g.t0) - own_lo;
+                            if (et < n_own) {
+                                const int c = own_lo + et;
+                                float2 acc2 = st_part[c];
+#pragma unroll
+                                for (int qq = 1; qq < 4; ++qq) {
+                                    const float2 v2 = st_part[qq * 256 + c];
+                                    acc2.x += v2.x;
+                                    acc2.y += v2.y;
+                                }
+                                op.stats_out[(int64_t)(g.t0 + c) * p.nft + g.f0 / 128] = acc2;
+                            }
                         }
-                        gemm_fixup(p, op, g, rb, re, ew, lane, mu_s, rs_s);
                     } else if (f32o && op.stats_out) {
                         // (sum, sumsq) of each row over this 128-feature tile: the 4
                         // lane quarters in a fixed order (deterministic)
-                        if (et < TN && g.t0 + et < p.M) {
+                        if (et < TNo && g.t0 + et < p.M) {
                             float2 acc2 = st_part[et];
 #pragma unroll
                             for (int qq = 1; qq < 4; ++qq) {
@@ -1100,41 +1159,61 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                         mbar_arrive(&p_full[b]);
                     }
                     J += a.nj;
-                    // partial (O_half, m, l) of this split -> workspace
+                    // merge the two key halves of each row inside the CTA: exchange
+                    // (m, l) through smem, then thread (row, half) combines dims
+                    // [half*HD/2, (half+1)*HD/2) of O_A and O_B from TMEM
+                    // (scratch overlaps the P tiles: only after the last PV completed)
                     mbar_wait(acc_full, nmma & 1);
                     if (et == 0) trace_ev(p, o, TR_ACC);
                     tc_fence_after();
+                    float* mlx = reinterpret_cast<float*>(smem + C::OFF_SCR);  // [2][2][128]
+                    mlx[(hh * 2 + 0) * 128 + i] = m_ref;
+                    mlx[(hh * 2 + 1) * 128 + i] = l;
+                    epi_bar();
+                    const float m0 = mlx[i], l0 = mlx[128 + i], m1 = mlx[256 + i], l1 = mlx[384 + i];
+                    const float mm = fmaxf(m0, m1);
+                    const float w0 = m0 == -INFINITY ? 0.f : ex2(m0 - mm);
+                    const float w1 = m1 == -INFINITY ? 0.f : ex2(m1 - mm);
+                    const float lsum = w0 * l0 + w1 * l1;
                     const int t = a.row0 + i;
-                    const int part = a.s * 2 + hh;
+                    const bool final_out = op.splits == 1;
+                    const float sc = final_out ? 1.0f / lsum : 1.0f;
+                    constexpr int DH = HD / 2;  // dims per thread
 #pragma unroll 1
-                    for (int cc = 0; cc < HD; cc += 32) {
-                        uint32_t ov[32];
-                        tmem_ld32(tOh + lane_off + cc, ov);
+                    for (int cc = 0; cc < DH; cc += 16) {
+                        uint32_t oa[16], ob[16];
+                        tmem_ld16(tbase + 128 + lane_off + hh * DH + cc, oa);
+                        tmem_ld16(tbase + 128 + HD + lane_off + hh * DH + cc, ob);
                         tmem_ld_wait();
-                        if (t < p.M && a.nj > 0) {
-                            float* dst = p.ws + ((int64_t)part * p.M + t) * p.kv + a.h * HD + cc;
+                        float v[16];
 #pragma unroll
-                            for (int e2 = 0; e2 < 32; e2 += 4)
-                                *reinterpret_cast<float4*>(dst + e2) =
-                                    make_float4(__uint_as_float(ov[e2]), __uint_as_float(ov[e2 + 1]),
-                                                __uint_as_float(ov[e2 + 2]), __uint_as_float(ov[e2 + 3]));
+                        for (int e2 = 0; e2 < 16; ++e2)
+                            v[e2] = (w0 * __uint_as_float(oa[e2]) + w1 * __uint_as_float(ob[e2])) * sc;
+                        if (t < p.M) {
+                            if (final_out) {
+                                __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(op.out) + (int64_t)t * p.kv + a.h * HD + hh * DH + cc;
+#pragma unroll
+                                for (int e2 = 0; e2 < 16; e2 += 4)
+                                    *reinterpret_cast<uint2*>(dst + e2) = pack_bf16x4(make_float4(v[e2], v[e2 + 1], v[e2 + 2], v[e2 + 3]));
+                            } else {
+                                float* dst = p.ws + ((int64_t)a.s * p.M + t) * p.kv + a.h * HD + hh * DH + cc;
+#pragma unroll
+                                for (int e2 = 0; e2 < 16; e2 += 4)
+                                    *reinterpret_cast<float4*>(dst + e2) = make_float4(v[e2], v[e2 + 1], v[e2 + 2], v[e2 + 3]);
+                            }
                         }
                     }
-                    if (t < p.M)
-                        p.wsml[((int64_t)part * p.M + t) * p.H + a.h] =
-                            a.nj > 0 ? make_float2(m_ref, l) : make_float2(-INFINITY, 0.f);
-                    if (a.nj == 0 && t < p.M) {
-                        float* dst = p.ws + ((int64_t)part * p.M + t) * p.kv + a.h * HD;
-                        for (int cc = 0; cc < HD; ++cc) dst[cc] = 0.f;
-                    }
+                    if (hh == 0 && t < p.M && !final_out) p.wsml[((int64_t)a.s * p.M + t) * p.H + a.h] = make_float2(mm, lsum);
                     tc_fence_before();
                     epi_bar();
                     if (et == 0) mbar_arrive(acc_empty);
                     ++nmma;
-                    split_meet(p, op, o, p.splitc + op.split_base + a.tile, et);
-                    const int rb = a.row0 + (a.s * 128) / op.splits;
-                    const int re = min(p.M, a.row0 + ((a.s + 1) * 128) / op.splits);
-                    attn_fixup<HD>(p, op, a, rb, re, ew, lane);
+                    if (!final_out) {
+                        split_meet(p, op, o, p.splitc + op.split_base + a.tile, et);
+                        const int rb = a.row0 + (a.s * 128) / op.splits;
+                        const int re = min(p.M, a.row0 + ((a.s + 1) * 128) / op.splits);
+                        attn_fixup<HD>(p, op, a, rb, re, ew, lane);
+                    }
                     publish(p, o, et);
                 }
             }

@@ -70,7 +70,11 @@ struct GemmCfg {
     static constexpr int W_BYTES = 128 * 64 * 2;
     static constexpr int X_BYTES = TN * 64 * 2;
     static constexpr int STAGE = W_BYTES + X_BYTES;
+#ifdef ALPA_GEMM_STAGES
+    static constexpr int STAGES = ALPA_GEMM_STAGES;
+#else
     static constexpr int STAGES = (200 * 1024) / STAGE > 8 ? 8 : (200 * 1024) / STAGE;
+#endif
     static constexpr int TAIL = 256 + 8 * 256;  // barriers + tmem slot + LN row stats
     static constexpr int SMEM = STAGES * STAGE + 1024 + TAIL;
     static constexpr uint32_t TCOLS = TN <= 32 ? 32 : TN <= 64 ? 64 : TN <= 128 ? 128 : 256;
