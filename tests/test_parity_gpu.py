@@ -280,3 +280,39 @@ def test_bf16_attention_kv_splits(port, monkeypatch, r, splits):
     err = rel_l2(res.actions, exp)
     print(f"bf16 attention r={r} splits={splits}: rel-L2 {err:.3e}")
     assert err <= BF16_TOL
+
+
+# ----------------------------------------------------------------- persistent kernel
+@pytest.mark.parametrize("n,B,K,r", [(6, 2, 2, 300), (3, 1, 1, 700)])
+def test_persistent_kernel_vs_per_op_path(port, monkeypatch, n, B, K, r):
+    """The persistent iteration kernel (default) and the per-op kernel sequence
+    (ALPA_MK=0) compute the same iteration: both within the bf16 bar of the
+    oracle, and each deterministic (graph replay == eager launch, bitwise).
+    Covers an odd lane count (partial 128-row query tile, half token tiles)
+    and a prefix that is not a multiple of the 64-key block."""
+    m = c2(B=B, K=K)
+    pre = port.synthetic_prefix(4242, B, r, m.kv_dim)
+    exp = port.refine(ocfg(m), port.weights(ocfg(m)), pre, port.noise(2, 1, n))
+    out = {}
+    for mk in ("1", "0"):
+        monkeypatch.setenv("ALPA_MK", mk)
+        with alpa.ActionGenerator(m) as g:
+            g.bind_prefix_synthetic(4242, r)
+            res = g.run_action_generation(alpa.InferenceRequest(num_trajectories=n, v0=5.0))
+            res_e = g.run_action_generation(alpa.InferenceRequest(num_trajectories=n, v0=5.0,
+                                                                  executor="eager"))
+        np.testing.assert_array_equal(res.actions, res_e.actions)
+        out[mk] = res.actions
+        err = rel_l2(res.actions, exp)
+        print(f"ALPA_MK={mk} n={n} B={B} K={K} r={r}: rel-L2 {err:.3e}")
+        assert err <= BF16_TOL
+    assert rel_l2(out["1"], out["0"]) <= BF16_TOL
+
+
+def test_persistent_kernel_single_launch_per_iteration(port):
+    """One persistent launch per denoising iteration (+ the rollout)."""
+    m = c2(B=2, K=3, action_hidden_dim=256, kv_dim=128, heads=1)
+    with alpa.ActionGenerator(m) as g:
+        g.bind_prefix(port.synthetic_prefix(7, 2, 100, 128))
+        res = g.run_action_generation(alpa.InferenceRequest(num_trajectories=6, v0=5.0))
+    assert res.stats["kernel_launches"] == 3 + 1
