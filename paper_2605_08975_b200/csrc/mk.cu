@@ -278,6 +278,13 @@ void mk_prepare(Ctx& c, int64_t n) {
     ALPA_CUDA(cudaMemcpy(m.d_ops, ops.data(), ops.size() * sizeof(Op), cudaMemcpyHostToDevice));
     m.counter_ints = (size_t)m.n_ops + split_ctr;
     m.d_counters = (int*)c.dalloc(m.counter_ints * sizeof(int));
+    if (getenv("ALPA_MK_DEBUG")) {  // plan dump (watchdog messages name counter addresses)
+        std::printf("mk plan: counters at %p (done[0..%d], split counters after)\n", (void*)m.d_counters,
+                    (int)ops.size());
+        for (size_t o = 0; o < ops.size(); ++o)
+            std::printf("  op %zu %s kind %d items %d splits %d tn %d dep %d/%d\n", o, tags[o], ops[o].kind,
+                        ops[o].n_items, ops[o].splits, ops[o].tn, ops[o].dep, ops[o].dep_count);
+    }
     ALPA_CUDA(cudaMemset(m.d_counters, 0, m.counter_ints * sizeof(int)));
     m.ws = (float*)c.dalloc(ws_floats * sizeof(float));
     m.wsml = (float2*)c.dalloc(wsml_elems * sizeof(float2));

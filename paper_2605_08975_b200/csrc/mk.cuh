@@ -182,7 +182,11 @@ __device__ __noinline__ void wait_count(const int* ctr, int want) {
     uint32_t n = 0;
     while (ld_relaxed(ctr) < want) {
         __nanosleep(64);
-        if (++n > (1u << 24)) __trap();
+        if (++n > (1u << 24)) {
+            printf("alpa mk watchdog: block %d thread %d waits counter %p = %d < %d\n", blockIdx.x, threadIdx.x,
+                   (const void*)ctr, ld_relaxed(ctr), want);
+            __trap();
+        }
     }
     (void)ld_acquire(ctr);
 }
