@@ -184,5 +184,7 @@ void prepare_iteration(Ctx& c, int64_t n);
 // tma.cu
 void make_tmap_bf16_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
                        uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer);
+void make_tmap_f32_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
+                      uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer);
 
 }  // namespace alpa

@@ -186,6 +186,16 @@ void mk_prepare(Ctx& c, int64_t n) {
         op.tmX = dm(act_map(xin, L.in, ttn));
         op.tmO = (out == c.ws.h1 || out == c.ws.qkv) ? dm(act_map(out, L.out, ttn)) : nullptr;
         op.tmXB = produce ? dm(act_map(c.ws.x, ah, ttn)) : nullptr;
+        if (op.splits > 1) {
+            // split finalisation: TN/S owned rows, fp32 e + bf16 copy via TMA stores
+            const int orows = ttn / op.splits;
+            CUtensorMap te{};
+            if ((size_t)orows * (512 + 256) <= (size_t)tn * 256 && orows % 8 == 0) {  // staging fits
+            make_tmap_f32_2d(&te, out, (uint64_t)L.out, (uint64_t)M, (uint64_t)ldo * 4, 128, (uint32_t)orows);
+            op.tmEs = dm(add_map(te));
+            if (produce) op.tmXs = dm(act_map(c.ws.x, ah, orows));
+            }
+        }
         op.bias = L.b;
         op.colsum = consume ? L.colsum : nullptr;
         op.out = out;
@@ -272,6 +282,8 @@ void mk_prepare(Ctx& c, int64_t n) {
         fix(op.tmQ);
         fix(op.tmO);
         fix(op.tmXB);
+        fix(op.tmEs);
+        fix(op.tmXs);
     }
     m.n_ops = (int)ops.size();
     m.d_ops = (Op*)c.dalloc(ops.size() * sizeof(Op));

@@ -59,6 +59,8 @@ struct Op {
     const CUtensorMap* tmQ;  // attention: qkv box {64,128}
     const CUtensorMap* tmO;  // GEMM, unsplit bf16 output: TMA store map, box {64,TN}
     const CUtensorMap* tmXB; // GEMM, unsplit residual producer: bf16 copy map, box {64,TN}
+    const CUtensorMap* tmEs; // GEMM, split residual producer: fp32 rows, box {128, TN/S}
+    const CUtensorMap* tmXs; // GEMM, split residual producer: bf16 copy, box {64, TN/S}
     const float* bias;
     const float* colsum;     // LN-folded consumers
     void* out;
@@ -126,7 +128,7 @@ struct Cfg {
     // epilogue staging of a bf16 [TN][128] output tile (two SW128 panels) +
     // scratch (LN mu/rstd, row-stat partials); shares the AUX region with the
     // attention Q and P tiles (ops are sequential within a CTA)
-    static constexpr int STG_BYTES = TN * 128 * 2;
+    static constexpr int STG_BYTES = TN * 128 * 2;  // also >= split rows x (512 + 256) B (S >= 4 at TN 192)
     static constexpr int SCR_BYTES = 12 * 1024;
     static constexpr int AUX_ATT = Q_BYTES + 2 * P_BYTES;
     static constexpr int AUX = AUX_ATT > STG_BYTES + SCR_BYTES ? AUX_ATT : STG_BYTES + SCR_BYTES;
@@ -444,9 +446,13 @@ struct FixArgs {
     const float* ws;          // workspace at (split 0, first owned token, feature)
     long long split_stride;   // floats between splits
     float bf;
-    float* erow;              // f32 output at the first owned token
-    __nv_bfloat16* xrow;      // bf16 copy or null
+    float* erow;              // direct stores (staging does not fit): f32 output at the first owned token
+    __nv_bfloat16* xrow;      //   and its bf16 copy (or null)
     long long ldo;
+    float* e_stg;             // fp32 staging [rows][128] (TMA store of the e rows), null: direct stores
+    uint8_t* x_stg;           // bf16 staging, SW128 panels of [rows][64] (null: no copy)
+    int rows;                 // owned rows of the tile (staging row count)
+    int r0;                   // this thread's first staging row
     float2* st_part;
 };
 template <bool RESID>
@@ -468,18 +474,34 @@ __device__ __forceinline__ void fix_t(const FixArgs& a) {
         for (int j = 0; j < 8; ++j) {
             float acc = 0.f;
 #pragma unroll
-            for (int s2 = 0; s2 < 4; ++s2)
+            for (int s2 = 0; s2 < 4; ++s2)  // fixed split order 0..S-1
                 if (s2 < a.S) acc += (s2 == a.s_own) ? __uint_as_float(r[j]) : pv[s2][j];
             float x = acc + a.bf;
             if constexpr (RESID) x = __uint_as_float(rv[j]) + x;
             v[j] = x;
         }
-        float* d = a.erow + (long long)c * a.ldo;
+        const int fl = a.q * 32 + a.lane;
+        if (!a.e_stg) {
+            float* d = a.erow + (long long)c * a.ldo;
 #pragma unroll
-        for (int j = 0; j < 8; ++j) stg(d + j * a.ldo, v[j]);
-        if (a.xrow) {
+            for (int j = 0; j < 8; ++j) stg(d + j * a.ldo, v[j]);
+            if (a.xrow) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) stg(a.xrow + (long long)(c + j) * a.ldo, v[j]);
+                for (int j = 0; j < 8; ++j) stg(a.xrow + (long long)(c + j) * a.ldo, v[j]);
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) a.e_stg[(a.r0 + c + j) * 128 + fl] = v[j];
+        }
+        if (a.e_stg && a.x_stg) {
+            const int col = fl & 63;
+            uint8_t* xb = a.x_stg + (fl >> 6) * (a.rows * 128) + (col & 7) * 2;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int row = a.r0 + c + j;
+                *reinterpret_cast<__nv_bfloat16*>(xb + row * 128 + ((((col >> 3) ^ (row & 7))) << 4)) =
+                    __float2bfloat16_rn(v[j]);
+            }
         }
         if (a.st_part) {
             float a1[8], a2[8];
@@ -1044,14 +1066,32 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                         fa.split_stride = (int64_t)p.M * op.nf;
                         fa.nf = op.nf;
                         fa.bf = op.bias[f];
+                        // outputs staged in smem, written by TMA tensor stores below
+                        const int orows = own_hi - own_lo;
+                        const bool staged = op.tmEs != nullptr;
                         fa.erow = reinterpret_cast<float*>(op.out) + (int64_t)(g.t0 + my_lo) * op.ldo + f;
                         fa.xrow = op.xb_out ? op.xb_out + (int64_t)(g.t0 + my_lo) * op.ldo + f : nullptr;
                         fa.ldo = op.ldo;
+                        fa.e_stg = staged ? reinterpret_cast<float*>(smem + C::OFF_STG) : nullptr;
+                        fa.x_stg = (staged && op.xb_out) ? smem + C::OFF_STG + orows * 512 : nullptr;
+                        fa.rows = orows;
+                        fa.r0 = my_lo - own_lo;
                         fa.st_part = op.stats_out ? st_part : nullptr;
                         fa.q = q;
                         fa.lane = lane;
                         if (resid) fix_t<true>(fa);
                         else fix_t<false>(fa);
+                        fence_proxy_async();
+                        epi_bar();
+                        if (staged && et == 0 && g.t0 + own_lo < p.M) {
+                            tma_store_2d(op.tmEs, smem + C::OFF_STG, g.f0, g.t0 + own_lo);
+                            if (op.xb_out) {
+                                tma_store_2d(op.tmXs, smem + C::OFF_STG + orows * 512, g.f0, g.t0 + own_lo);
+                                tma_store_2d(op.tmXs, smem + C::OFF_STG + orows * 512 + orows * 128, g.f0 + 64,
+                                             g.t0 + own_lo);
+                            }
+                            bulk_commit();
+                        }
                         if (op.stats_out) {
                             epi_bar();
                             const int n_own = min(own_hi, p.M - g.t0) - own_lo;

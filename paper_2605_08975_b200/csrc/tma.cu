@@ -35,4 +35,20 @@ void make_tmap_bf16_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_
         fail(ALPA_ERR_INTERNAL, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
 }
 
+// 2-D fp32 row-major tensor [outer][inner], box {box_inner (<= 256), box_outer},
+// no swizzle (epilogue TMA stores of fp32 rows staged row-major in smem).
+void make_tmap_f32_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
+                      uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer) {
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {row_stride_bytes};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims,
+                             strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        fail(ALPA_ERR_INTERNAL, "cuTensorMapEncodeTiled (f32) failed (" + std::to_string((int)r) + ")");
+}
+
 }  // namespace alpa

@@ -7,11 +7,15 @@ using namespace alpa;
 
 struct Bufs { void *W, *X, *out, *xb; float *bias, *colsum; float2* stats; };
 
+static int g_copies = 1;  // >1: rotate through weight copies (larger than L2 -> cold weights)
 template <int TN, int EPI>
 float run(int nf, int T, int K, int splits, const Bufs& b) {
     using Cf = GemmCfg<TN>;
     cudaFuncSetAttribute(tc_gemm_kernel<TN, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cf::SMEM);
     CUtensorMap tw, tx;
+    CUtensorMap twc[8];
+    for (int c = 0; c < g_copies; ++c)
+        make_tmap_bf16_2d(&twc[c], (uint8_t*)b.W + (size_t)c * 8192 * 8192 * 2, K, nf, K * 2, 64, 128);
     make_tmap_bf16_2d(&tw, b.W, K, nf, K * 2, 64, 128);
     make_tmap_bf16_2d(&tx, b.X, K, T, K * 2, 64, TN);
     GemmArgs a{};
@@ -28,7 +32,7 @@ float run(int nf, int T, int K, int splits, const Bufs& b) {
     for (int i = 0; i < 3; ++i) cudaLaunchKernelEx(&cfg, tc_gemm_kernel<TN, EPI>, tw, tx, a);
     cudaEventRecord(e0);
     const int R = 50;
-    for (int i = 0; i < R; ++i) cudaLaunchKernelEx(&cfg, tc_gemm_kernel<TN, EPI>, tw, tx, a);
+    for (int i = 0; i < R; ++i) cudaLaunchKernelEx(&cfg, tc_gemm_kernel<TN, EPI>, g_copies > 1 ? twc[i % g_copies] : tw, tx, a);
     cudaEventRecord(e1); cudaEventSynchronize(e1);
     float ms; cudaEventElapsedTime(&ms, e0, e1);
     cudaError_t e = cudaGetLastError();
@@ -36,12 +40,13 @@ float run(int nf, int T, int K, int splits, const Bufs& b) {
     return ms / R * 1000.f;
 }
 
-int main() {
+int main(int argc, char** argv) {
     Bufs b;
-    cudaMalloc(&b.W, (size_t)8192 * 8192 * 2); cudaMalloc(&b.X, (size_t)4096 * 8192 * 2);
+    if (argc > 1) g_copies = atoi(argv[1]);
+    cudaMalloc(&b.W, (size_t)8192 * 8192 * 2 * (g_copies > 1 ? 8 : 1)); cudaMalloc(&b.X, (size_t)4096 * 8192 * 2);
     cudaMalloc(&b.out, (size_t)4096 * 8192 * 4); cudaMalloc(&b.xb, (size_t)4096 * 8192 * 2);
     cudaMalloc(&b.bias, 8192 * 4); cudaMalloc(&b.colsum, 8192 * 4); cudaMalloc(&b.stats, 4096 * 16 * 8);
-    cudaMemset(b.W, 0, (size_t)8192 * 8192 * 2); cudaMemset(b.X, 0, (size_t)4096 * 8192 * 2);
+    cudaMemset(b.W, 0, (size_t)8192 * 8192 * 2 * (g_copies > 1 ? 8 : 1)); cudaMemset(b.X, 0, (size_t)4096 * 8192 * 2);
     cudaMemset(b.bias, 0, 8192 * 4); cudaMemset(b.colsum, 0, 8192 * 4); cudaMemset(b.stats, 0, 4096 * 16 * 8);
     cudaMemset(b.out, 0, (size_t)4096 * 8192 * 4);
     printf("mlp1 (8192x384x2048, S=1): none %6.1f  bf16 %6.1f  gelu %6.1f  ln_gelu %6.1f  f32 %6.1f resid %6.1f us\n",
