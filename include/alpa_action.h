@@ -100,7 +100,13 @@ typedef struct alpa_stats {
     int64_t kv_bytes;            /* footprint_bytes() equivalent (kv_cache.cpp:365)*/
     int64_t h2d_bytes;
     int64_t d2h_bytes;
+    /* per diffusion iteration device time (LatencyReport::action_gen_iter_ms,
+     * profiler.hpp:36): events between the iterations, inside the graph too */
+    int64_t n_iter;              /* iterations recorded (<= ALPA_MAX_ITER_MS)    */
+    double iter_ms[64];
+    int64_t bytes_allocated;     /* device bytes owned by the context            */
 } alpa_stats;
+#define ALPA_MAX_ITER_MS 64
 
 /* ---- context ------------------------------------------------------------ */
 int alpa_ctx_create(const alpa_model_cfg* cfg, int device, alpa_ctx** out);
@@ -173,6 +179,17 @@ int alpa_profile(alpa_ctx* ctx, const alpa_request* req, int64_t iters, alpa_ker
  * 7 accumulator drained, 8 fixup done, 9 publish fences passed. */
 int alpa_debug_mk_trace(alpa_ctx* ctx, unsigned long long* out, int64_t max_elems,
                         int64_t* n_ops, int64_t* grid);
+
+/* ---- open-loop evaluation (eval.cpp:14-59), bit-exact fp64 -------------- */
+/* Batch of scenes: traj [scenes][n][steps][3] (x, y, yaw), gt [scenes][steps][3];
+ * outputs min_ade [scenes] (minivla::min_ade) and diversity [scenes]
+ * (minivla::diversity); either output may be NULL.  Errors like the reference:
+ * n < 1 -> ALPA_ERR_INTERNAL ("min_ade: no samples"), diversity with n < 2 ->
+ * ALPA_ERR_INTERNAL.  Host-buffer variant and device-pointer variant. */
+int alpa_eval_open_loop(alpa_ctx* ctx, const float* traj, const float* gt, int64_t scenes, int64_t n,
+                        int64_t steps, double* min_ade, double* diversity);
+int alpa_eval_open_loop_device(alpa_ctx* ctx, const float* d_traj, const float* d_gt, int64_t scenes,
+                               int64_t n, int64_t steps, double* d_min_ade, double* d_diversity);
 
 /* ---- host helpers (bit-exact restatements of the reference host code) -- */
 /* Rng::normal noise for lanes [lane0, lane0+n): out [n][steps][2]. */

@@ -15,6 +15,8 @@
 #pragma once
 
 #include <array>
+#include <cstdio>
+#include <string>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -137,6 +139,43 @@ struct DiffusionResult {
     double device_ms = 0.0;
 };
 
+// minivla::LatencyReport (profiler.hpp:31-46) and its JSON wire format
+// (profiler.cpp:31-46: same keys, numbers printed round-trip exact).
+struct LatencyReport {
+    std::array<double, 5> component_ms{};  // preprocessing, reasoning vision/prefill/decode, action gen
+    double total_ms = 0.0;
+    double postprocessing_ms = 0.0;
+    int repeats = 1;
+    std::vector<double> action_gen_iter_ms;
+    std::uint64_t alloc_count = 0;
+    std::uint64_t dispatch_count = 0;
+    std::uint64_t replay_count = 0;
+    std::uint64_t bytes_allocated = 0;
+    std::int64_t kv_bytes = 0;
+    std::int64_t cot_tokens = 0;
+
+    std::string to_json() const {
+        static const char* keys[5] = {"preprocessing_ms", "reasoning_vision_ms", "reasoning_prefill_ms",
+                                      "reasoning_decode_ms", "action_gen_ms"};
+        auto num = [](double v) {
+            char b[40];
+            std::snprintf(b, sizeof b, "%.17g", v);
+            return std::string(b);
+        };
+        std::string j = "{";
+        for (int i = 0; i < 5; ++i) j += "\"" + std::string(keys[i]) + "\":" + num(component_ms[i]) + ",";
+        j += "\"total_ms\":" + num(total_ms) + ",\"postprocessing_ms\":" + num(postprocessing_ms) +
+             ",\"repeats\":" + std::to_string(repeats) + ",\"action_gen_iter_ms\":[";
+        for (size_t i = 0; i < action_gen_iter_ms.size(); ++i)
+            j += (i ? "," : "") + num(action_gen_iter_ms[i]);
+        j += "],\"alloc_count\":" + std::to_string(alloc_count) + ",\"dispatch_count\":" +
+             std::to_string(dispatch_count) + ",\"replay_count\":" + std::to_string(replay_count) +
+             ",\"bytes_allocated\":" + std::to_string(bytes_allocated) + ",\"kv_bytes\":" +
+             std::to_string(kv_bytes) + ",\"cot_tokens\":" + std::to_string(cot_tokens) + "}";
+        return j;
+    }
+};
+
 inline float initial_speed_from_history(const PoseHistory& h) {  // pipeline.cpp:150-156
     float buf[16 * 3];
     for (int i = 0; i < 16; ++i) {
@@ -176,9 +215,10 @@ public:
         alpa_stats st{};
         check(alpa_generate(ctx_, &r, acts.data(), nullptr, &st), ctx_);
         if (kv_bytes) *kv_bytes = st.kv_bytes;
+        last_stats_ = st;
         if (diff) {
-            diff->iter_ms.assign(static_cast<size_t>(cfg_.diffusion_iters),
-                                 st.device_ms / static_cast<double>(cfg_.diffusion_iters));
+            // per-iteration device times (timing events between the iterations)
+            diff->iter_ms.assign(st.iter_ms, st.iter_ms + st.n_iter);
             diff->graph_commands = st.graph_nodes;
             diff->graph_launches = st.graph_launches;
             diff->device_ms = st.device_ms;
@@ -236,7 +276,56 @@ public:
         return t;
     }
 
+    // minivla::min_ade / minivla::diversity (eval.cpp:39-59) on the device, bit-exact.
+    double min_ade(const std::vector<Trajectory>& samples, const Trajectory& gt) {
+        std::vector<float> t = flatten(samples), g = flatten({gt});
+        double out = 0.0;
+        check(alpa_eval_open_loop(ctx_, t.data(), g.data(), 1, static_cast<std::int64_t>(samples.size()),
+                                  static_cast<std::int64_t>(gt.poses.size()), &out, nullptr),
+              ctx_);
+        return out;
+    }
+    double diversity(const std::vector<Trajectory>& samples) {
+        std::vector<float> t = flatten(samples);
+        const std::int64_t steps = samples.empty() ? 0 : static_cast<std::int64_t>(samples[0].poses.size());
+        double out = 0.0;
+        check(alpa_eval_open_loop(ctx_, t.data(), nullptr, 1, static_cast<std::int64_t>(samples.size()), steps,
+                                  nullptr, &out),
+              ctx_);
+        return out;
+    }
+
+    // LatencyReport (profiler.hpp:31-46, profiler.cpp:31-46 key set) of the last
+    // run_action_generation: the action-generation component and its counters;
+    // the reasoning / preprocessing components belong to stages outside this path.
+    LatencyReport latency_report() const {
+        LatencyReport r;
+        r.component_ms[4] = last_stats_.device_ms;  // LatencyComponent::ActionGen
+        r.total_ms = last_stats_.device_ms;
+        r.action_gen_iter_ms.assign(last_stats_.iter_ms, last_stats_.iter_ms + last_stats_.n_iter);
+        r.alloc_count = 0;  // every buffer is allocated before the first launch
+        r.dispatch_count = static_cast<std::uint64_t>(last_stats_.kernel_launches);
+        r.replay_count = static_cast<std::uint64_t>(last_stats_.graph_launches);
+        r.bytes_allocated = static_cast<std::uint64_t>(last_stats_.bytes_allocated);
+        r.kv_bytes = last_stats_.kv_bytes;
+        return r;
+    }
+
 private:
+    alpa_stats last_stats_{};
+    static std::vector<float> flatten(const std::vector<Trajectory>& ts) {
+        std::vector<float> out;
+        for (const Trajectory& t : ts) {
+            if (!ts.empty() && t.poses.size() != ts[0].poses.size())
+                throw InternalError("trajectory length mismatch");  // eval.cpp:15-17
+            for (const Pose& p : t.poses) {
+                out.push_back(p.x);
+                out.push_back(p.y);
+                out.push_back(p.yaw);
+            }
+        }
+        return out;
+    }
     void bind(const ReasoningOutput& r) {
         if (bound_version_ == r.version && bound_ptr_ == &r) return;
         if (r.kv_device)

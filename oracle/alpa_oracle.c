@@ -409,3 +409,42 @@ int64_t orc_kv_footprint_bytes(int64_t blocks, int64_t batch, int64_t tokens,
                                int64_t kv_dim, int64_t elem_bytes) {
     return blocks * batch * tokens * kv_dim * 2 * elem_bytes;
 }
+
+/* --------------------------------------------------------------- open-loop metrics */
+
+static double mean_displacement(const float* a, const float* b, int64_t steps) {
+    /* eval.cpp:14-25: double accumulation in pose order (no FMA: -ffp-contract=off) */
+    double sum = 0.0;
+    for (int64_t i = 0; i < steps; ++i) {
+        const double dx = (double)a[i * 3] - (double)b[i * 3];
+        const double dy = (double)a[i * 3 + 1] - (double)b[i * 3 + 1];
+        sum += sqrt(dx * dx + dy * dy);
+    }
+    return sum / (double)steps;
+}
+
+int orc_min_ade(const float* traj, int64_t n, int64_t steps, const float* gt, double* out) {
+    /* eval.cpp:39-46 */
+    if (n < 1) return 3;
+    double best = mean_displacement(traj, gt, steps);
+    for (int64_t i = 1; i < n; ++i) {
+        const double d = mean_displacement(traj + i * steps * 3, gt, steps);
+        best = d < best ? d : best; /* std::min(best, d) */
+    }
+    *out = best;
+    return 0;
+}
+
+int orc_diversity(const float* traj, int64_t n, int64_t steps, double* out) {
+    /* eval.cpp:48-59 */
+    if (n < 2) return 3;
+    double sum = 0.0;
+    int64_t pairs = 0;
+    for (int64_t i = 0; i < n; ++i)
+        for (int64_t j = i + 1; j < n; ++j) {
+            sum += mean_displacement(traj + i * steps * 3, traj + j * steps * 3, steps);
+            pairs += 1;
+        }
+    *out = sum / (double)pairs;
+    return 0;
+}

@@ -97,6 +97,15 @@ int orc_diffusion_refine(const orc_cfg* c, const orc_weights* w, const float* pr
  * Returns 3 (InternalError) on bad speed / non-finite actions. */
 int orc_rollout(const float* actions, int64_t n, int64_t steps, float v0, float* traj);
 
+/* Open-loop metrics (eval.cpp:14-59): trajectories traj [n][steps][3] (x, y, yaw;
+ * only x, y used), ground truth gt [steps][3].  mean_displacement is the mean of
+ * sqrt(dx^2 + dy^2) over the poses in double, summed in pose order
+ * (eval.cpp:14-25); min_ade = min over samples in sample order (eval.cpp:39-46);
+ * diversity = mean over pairs i < j in row-major pair order (eval.cpp:48-59).
+ * Return 3 (InternalError) for n < 1 (min_ade) / n < 2 (diversity). */
+int orc_min_ade(const float* traj, int64_t n, int64_t steps, const float* gt, double* out);
+int orc_diversity(const float* traj, int64_t n, int64_t steps, double* out);
+
 /* initial_speed_from_history (pipeline.cpp:150-156); history [16][3]. */
 float orc_initial_speed(const float* history);
 

@@ -102,6 +102,8 @@ class Port:
         L.orc_diffusion_refine.argtypes = [C.POINTER(Cfg), C.POINTER(_Weights), _f32p, C.c_int64,
                                            _i32p, C.c_int64, C.c_int64, _f32p, C.c_int]
         L.orc_rollout.argtypes = [_f32p, C.c_int64, C.c_int64, C.c_float, _f32p]
+        L.orc_min_ade.argtypes = [_f32p, C.c_int64, C.c_int64, _f32p, C.POINTER(C.c_double)]
+        L.orc_diversity.argtypes = [_f32p, C.c_int64, C.c_int64, C.POINTER(C.c_double)]
         L.orc_initial_speed.restype = C.c_float
         L.orc_initial_speed.argtypes = [_f32p]
         L.orc_fnv1a.restype = C.c_uint64
@@ -164,6 +166,21 @@ class Port:
             raise ValueError("actions_to_trajectory: invalid input (InternalError)")
         return out
 
+    def min_ade(self, traj: np.ndarray, gt: np.ndarray) -> float:
+        t = np.ascontiguousarray(traj, np.float32)
+        g = np.ascontiguousarray(gt, np.float32)
+        out = C.c_double()
+        if self.L.orc_min_ade(_fp(t), t.shape[0], t.shape[1], _fp(g), C.byref(out)):
+            raise ValueError("min_ade: no samples (InternalError)")
+        return out.value
+
+    def diversity(self, traj: np.ndarray) -> float:
+        t = np.ascontiguousarray(traj, np.float32)
+        out = C.c_double()
+        if self.L.orc_diversity(_fp(t), t.shape[0], t.shape[1], C.byref(out)):
+            raise ValueError("diversity: need at least 2 samples (InternalError)")
+        return out.value
+
     def initial_speed(self, history: np.ndarray) -> float:
         h = np.ascontiguousarray(history, np.float32)
         return float(self.L.orc_initial_speed(_fp(h)))
@@ -224,6 +241,9 @@ class Ref:
         L.ref_rollout.argtypes = [_f32p, C.c_int64, C.c_float, _f32p]
         L.ref_action_weights.argtypes = [C.POINTER(Cfg), C.c_int, _f32p, C.c_int64,
                                          C.POINTER(C.c_int64)]
+        L.ref_parse_latency_report.argtypes = [C.c_char_p, C.POINTER(C.c_int64), C.POINTER(C.c_double)]
+        L.ref_min_ade.argtypes = [_f32p, C.c_int64, C.c_int64, _f32p, C.POINTER(C.c_double)]
+        L.ref_diversity.argtypes = [_f32p, C.c_int64, C.c_int64, C.POINTER(C.c_double)]
         self.L = L
 
     def _check(self, rc):
@@ -264,6 +284,26 @@ class Ref:
         out = np.empty((n, 64, 3), np.float32)
         self._check(self.L.ref_rollout(_fp(actions), n, v0, _fp(out)))
         return out
+
+    def parse_latency_report(self, doc: str) -> tuple[int, float]:
+        """LatencyReport::from_json of the reference (profiler.cpp:49-66)."""
+        n = C.c_int64()
+        ms = C.c_double()
+        self._check(self.L.ref_parse_latency_report(doc.encode(), C.byref(n), C.byref(ms)))
+        return n.value, ms.value
+
+    def min_ade(self, traj: np.ndarray, gt: np.ndarray) -> float:
+        t = np.ascontiguousarray(traj, np.float32)
+        g = np.ascontiguousarray(gt, np.float32)
+        out = C.c_double()
+        self._check(self.L.ref_min_ade(_fp(t), t.shape[0], t.shape[1], _fp(g), C.byref(out)))
+        return out.value
+
+    def diversity(self, traj: np.ndarray) -> float:
+        t = np.ascontiguousarray(traj, np.float32)
+        out = C.c_double()
+        self._check(self.L.ref_diversity(_fp(t), t.shape[0], t.shape[1], C.byref(out)))
+        return out.value
 
     def action_weight(self, cfg: Cfg, which: int) -> np.ndarray:
         cnt = C.c_int64()

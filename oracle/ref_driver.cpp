@@ -17,6 +17,8 @@
 // No reference source is copied here; everything is a call into it.
 
 #include "minivla/common.hpp"
+#include "minivla/eval.hpp"
+#include "minivla/profiler.hpp"
 #include "minivla/kv_cache.hpp"
 #include "minivla/model.hpp"
 #include "minivla/pipeline.hpp"
@@ -26,6 +28,7 @@
 #include <cstdint>
 #include <cstring>
 #include <string>
+#include <span>
 #include <vector>
 
 using namespace minivla;
@@ -259,6 +262,41 @@ int ref_action_weights(const RefCfg* c, int which, float* out, std::int64_t cap,
             if (cap < *count_out) throw InternalError("buffer too small");
             std::memcpy(out, src->data(), src->size() * sizeof(float));
         }
+    });
+}
+
+// LatencyReport::from_json of the reference on a JSON document (wire-format
+// check of the shim's report); writes back the number of iteration entries.
+int ref_parse_latency_report(const char* json, std::int64_t* n_iter, double* action_gen_ms) {
+    return guarded([&] {
+        const LatencyReport r = LatencyReport::from_json(nlohmann::json::parse(json));
+        *n_iter = static_cast<std::int64_t>(r.action_gen_iter_ms.size());
+        *action_gen_ms = r.component_ms[static_cast<int>(LatencyComponent::ActionGen)];
+    });
+}
+
+// minivla::min_ade / minivla::diversity (eval.cpp:39-59) on [n][64][3] poses.
+static std::vector<Trajectory> to_trajs(const float* traj, std::int64_t n, std::int64_t steps) {
+    std::vector<Trajectory> out(static_cast<std::size_t>(n));
+    for (std::int64_t l = 0; l < n; ++l) {
+        out[l].poses.resize(steps);
+        for (std::int64_t i = 0; i < steps; ++i)
+            out[l].poses[i] = {traj[(l * steps + i) * 3], traj[(l * steps + i) * 3 + 1],
+                               traj[(l * steps + i) * 3 + 2]};
+    }
+    return out;
+}
+int ref_min_ade(const float* traj, std::int64_t n, std::int64_t steps, const float* gt, double* out) {
+    return guarded([&] {
+        const std::vector<Trajectory> s = to_trajs(traj, n, steps);
+        const std::vector<Trajectory> g = to_trajs(gt, 1, steps);
+        *out = min_ade(std::span<const Trajectory>(s), g[0]);
+    });
+}
+int ref_diversity(const float* traj, std::int64_t n, std::int64_t steps, double* out) {
+    return guarded([&] {
+        const std::vector<Trajectory> s = to_trajs(traj, n, steps);
+        *out = diversity(std::span<const Trajectory>(s));
     });
 }
 

@@ -79,11 +79,14 @@ class Stats(C.Structure):
     _fields_ = [
         ("device_ms", C.c_double), ("kernel_launches", C.c_int64), ("graph_launches", C.c_int64),
         ("graph_nodes", C.c_int64), ("kv_bytes", C.c_int64), ("h2d_bytes", C.c_int64),
-        ("d2h_bytes", C.c_int64),
+        ("d2h_bytes", C.c_int64), ("n_iter", C.c_int64), ("iter_ms", C.c_double * 64),
+        ("bytes_allocated", C.c_int64),
     ]
 
     def as_dict(self) -> dict:
-        return {k: getattr(self, k) for k, _ in self._fields_}
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k != "iter_ms"}
+        d["iter_ms"] = [self.iter_ms[i] for i in range(min(self.n_iter, 64))]
+        return d
 
 
 class KernelProf(C.Structure):
@@ -136,6 +139,11 @@ def lib():
         L.alpa_rollout.argtypes = [C.c_void_p, _f32p, C.c_int64, C.c_float, _f32p]
         L.alpa_kv_footprint_bytes.restype = C.c_int64
         L.alpa_kv_footprint_bytes.argtypes = [C.c_int64] * 5
+        _f64p = C.POINTER(C.c_double)
+        L.alpa_eval_open_loop.argtypes = [C.c_void_p, _f32p, _f32p, C.c_int64, C.c_int64, C.c_int64,
+                                          _f64p, _f64p]
+        L.alpa_eval_open_loop_device.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                                 C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]
         _lib = L
     return _lib
 
@@ -315,6 +323,27 @@ class ActionGenerator:
         return [dict(name=buf[i].name.decode(), launches=buf[i].launches,
                      total_ms=buf[i].total_ms, flops=buf[i].flops, bytes=buf[i].bytes)
                 for i in range(n.value)]
+
+    def eval_open_loop(self, traj: np.ndarray, gt: np.ndarray | None = None,
+                       diversity: bool = True) -> tuple[np.ndarray, np.ndarray | None]:
+        """minivla::min_ade / minivla::diversity (eval.cpp:39-59) of a batch of scenes on
+        the device, bit-exact: traj [scenes][n][steps][3] (or [n][steps][3]), gt
+        [scenes][steps][3] (or [steps][3]).  Returns (min_ade [scenes], diversity
+        [scenes] or None)."""
+        t = np.ascontiguousarray(traj, np.float32)
+        if t.ndim == 3:
+            t = t[None]
+        scenes, n, steps = t.shape[0], t.shape[1], t.shape[2]
+        g = None
+        if gt is not None:
+            g = np.ascontiguousarray(gt, np.float32).reshape(scenes, steps, 3)
+        ade = np.empty(scenes, np.float64)
+        div = np.empty(scenes, np.float64) if diversity else None
+        f64 = lambda a: a.ctypes.data_as(C.POINTER(C.c_double)) if a is not None else None  # noqa: E731
+        _check(lib().alpa_eval_open_loop(self._h, _fp(t), _fp(g) if g is not None else None, scenes,
+                                         n, steps, f64(ade) if g is not None else None, f64(div)),
+               self._h)
+        return (ade if g is not None else None), div
 
     def rollout(self, actions: np.ndarray, v0: float) -> np.ndarray:
         a = np.ascontiguousarray(actions, np.float32)

@@ -128,6 +128,24 @@ void upload_lane_map(Ctx& c, const alpa_request& r) {
                               c.stream));
 }
 
+// Timing events between the iterations (recorded as external event nodes
+// when the loop is captured, so they time the graph replay too).
+void iter_events(Ctx& c, int64_t K) {
+    const int64_t need = std::min<int64_t>(K, ALPA_MAX_ITER_MS) + 1;
+    while ((int64_t)c.iter_ev.size() < need) {
+        cudaEvent_t e;
+        ALPA_CUDA(cudaEventCreate(&e));
+        c.iter_ev.push_back(e);
+    }
+}
+void record_iter(Ctx& c, int64_t k, cudaStream_t s, bool capturing) {
+    if (k >= (int64_t)c.iter_ev.size()) return;
+    if (capturing)  // an event-record node of the graph, usable for timing
+        ALPA_CUDA(cudaEventRecordWithFlags(c.iter_ev[k], s, cudaEventRecordExternal));
+    else
+        ALPA_CUDA(cudaEventRecord(c.iter_ev[k], s));
+}
+
 // Runs the whole K loop + rollout on c.ws buffers (actions already there).
 // Graph executor: the K iterations and the rollout are ONE captured CUDA
 // graph (model.cpp:607-636 captures one iteration and replays it K-2 times;
@@ -145,8 +163,13 @@ void run_loop(Ctx& c, const alpa_request& r, int64_t K, alpa_stats* st) {
             cudaGraph_t g = nullptr;
             ALPA_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
             c.last_launches = 0;
+            iter_events(c, K);
             try {
-                for (int64_t it = 0; it < K; ++it) alpa::enqueue_iteration(c, n, s);
+                record_iter(c, 0, s, true);
+                for (int64_t it = 0; it < K; ++it) {
+                    alpa::enqueue_iteration(c, n, s);
+                    record_iter(c, it + 1, s, true);
+                }
                 alpa::enqueue_rollout(c, n, c.ws.actions, c.ws.traj, s);
             } catch (...) {
                 cudaStreamEndCapture(s, &g);
@@ -168,7 +191,12 @@ void run_loop(Ctx& c, const alpa_request& r, int64_t K, alpa_stats* st) {
         }
     } else {
         c.last_launches = 0;
-        for (int64_t it = 0; it < K; ++it) alpa::enqueue_iteration(c, n, s);
+        iter_events(c, K);
+        record_iter(c, 0, s, false);
+        for (int64_t it = 0; it < K; ++it) {
+            alpa::enqueue_iteration(c, n, s);
+            record_iter(c, it + 1, s, false);
+        }
         alpa::enqueue_rollout(c, n, c.ws.actions, c.ws.traj, s);
         if (st) {
             st->graph_launches = 0;
@@ -176,6 +204,19 @@ void run_loop(Ctx& c, const alpa_request& r, int64_t K, alpa_stats* st) {
             st->kernel_launches = c.last_launches;
         }
     }
+    c.iter_ev_used = std::min<int64_t>(K, ALPA_MAX_ITER_MS);
+}
+
+// After the stream synchronised: per-iteration times into the stats.
+void fill_iter_ms(Ctx& c, alpa_stats* st) {
+    if (!st) return;
+    st->n_iter = c.iter_ev_used;
+    for (int64_t k = 0; k < c.iter_ev_used; ++k) {
+        float ms = 0.f;
+        ALPA_CUDA(cudaEventElapsedTime(&ms, c.iter_ev[k], c.iter_ev[k + 1]));
+        st->iter_ms[k] = ms;
+    }
+    st->bytes_allocated = (int64_t)c.dev_bytes;
 }
 
 int64_t kv_bytes(const Ctx& c, const alpa_request& r) {
@@ -266,6 +307,7 @@ void alpa_ctx_destroy(alpa_ctx* h) {
     if (c->pinned) cudaFreeHost(c->pinned);
     if (c->ev0) cudaEventDestroy(c->ev0);
     if (c->ev1) cudaEventDestroy(c->ev1);
+    for (cudaEvent_t e : c->iter_ev) cudaEventDestroy(e);
     if (c->own_stream && c->stream) cudaStreamDestroy(c->stream);
     delete c;
 }
@@ -427,6 +469,7 @@ int alpa_generate(alpa_ctx* h, const alpa_request* req, float* actions_out, floa
             float ms = 0.f;
             cudaEventElapsedTime(&ms, c->ev0, c->ev1);
             st->device_ms = ms;
+            fill_iter_ms(*c, st);
             st->kv_bytes = kv_bytes(*c, r);
             st->h2d_bytes = (int64_t)(na * sizeof(float));
             st->d2h_bytes = (int64_t)((na + nt) * sizeof(float));
@@ -464,6 +507,7 @@ int alpa_generate_device(alpa_ctx* h, const alpa_request* req, const float* d_no
             float ms = 0.f;
             cudaEventElapsedTime(&ms, c->ev0, c->ev1);
             st->device_ms = ms;
+            fill_iter_ms(*c, st);
             st->kv_bytes = kv_bytes(*c, r);
         }
     });
@@ -553,6 +597,50 @@ int alpa_debug_mk_trace(alpa_ctx* h, unsigned long long* out, int64_t max_elems,
         ALPA_CUDA(cudaMemcpy(out, c->mk.d_trace, n * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
         *n_ops = c->mk.n_ops;
         *grid = c->mk.grid;
+    });
+}
+
+int alpa_eval_open_loop_device(alpa_ctx* h, const float* d_traj, const float* d_gt, int64_t scenes,
+                               int64_t n, int64_t steps, double* d_min_ade, double* d_diversity) {
+    Ctx* c = reinterpret_cast<Ctx*>(h);
+    return guarded(c, [&] {
+        if (!c || !d_traj) fail(ALPA_ERR_CONFIG, "null argument");
+        cudaSetDevice(c->device);
+        alpa::eval_open_loop_device(*c, d_traj, d_gt, scenes, n, steps, d_min_ade, d_diversity, c->stream);
+    });
+}
+
+int alpa_eval_open_loop(alpa_ctx* h, const float* traj, const float* gt, int64_t scenes, int64_t n,
+                        int64_t steps, double* min_ade, double* diversity) {
+    Ctx* c = reinterpret_cast<Ctx*>(h);
+    return guarded(c, [&] {
+        if (!c || !traj) fail(ALPA_ERR_CONFIG, "null argument");
+        cudaSetDevice(c->device);
+        if (n < 1) fail(ALPA_ERR_INTERNAL, "min_ade: no samples");
+        if (diversity && n < 2) fail(ALPA_ERR_INTERNAL, "diversity: need at least 2 samples");
+        if (scenes < 1) return;
+        const size_t tb = (size_t)(scenes * n * steps * 3) * sizeof(float);
+        const size_t gb = gt ? (size_t)(scenes * steps * 3) * sizeof(float) : 0;
+        const size_t ob = (size_t)scenes * sizeof(double);
+        uint8_t* d = nullptr;
+        ALPA_CUDA(cudaMalloc(&d, tb + gb + 2 * ob + 64));
+        float* dt = reinterpret_cast<float*>(d);
+        float* dg = gt ? reinterpret_cast<float*>(d + tb) : nullptr;
+        double* dm = reinterpret_cast<double*>(d + ((tb + gb + 15) & ~(size_t)15));
+        double* dv = dm + scenes;
+        try {
+            ALPA_CUDA(cudaMemcpyAsync(dt, traj, tb, cudaMemcpyHostToDevice, c->stream));
+            if (gt) ALPA_CUDA(cudaMemcpyAsync(dg, gt, gb, cudaMemcpyHostToDevice, c->stream));
+            alpa::eval_open_loop_device(*c, dt, dg, scenes, n, steps, min_ade ? dm : nullptr,
+                                        diversity ? dv : nullptr, c->stream);
+            if (min_ade) ALPA_CUDA(cudaMemcpyAsync(min_ade, dm, ob, cudaMemcpyDeviceToHost, c->stream));
+            if (diversity) ALPA_CUDA(cudaMemcpyAsync(diversity, dv, ob, cudaMemcpyDeviceToHost, c->stream));
+            ALPA_CUDA(cudaStreamSynchronize(c->stream));
+        } catch (...) {
+            cudaFree(d);
+            throw;
+        }
+        cudaFree(d);
     });
 }
 

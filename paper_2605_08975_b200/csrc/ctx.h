@@ -141,6 +141,11 @@ struct Ctx {
     std::vector<ProfRec> prof;
     std::vector<cudaEvent_t> ev_pool;
     size_t ev_next = 0;
+    std::vector<cudaEvent_t> iter_ev;  // K+1 timing events around the iterations
+    int64_t iter_ev_used = 0;
+    size_t dev_bytes = 0;              // device bytes allocated by the context
+    void* eval_scratch = nullptr;  // eval.cu: per-(scene, term) mean displacements
+    size_t eval_scratch_bytes = 0;
 
     bool bf16() const { return cfg.dtype == ALPA_DTYPE_BF16; }
     int64_t ah() const { return cfg.action_hidden_dim; }
@@ -152,6 +157,7 @@ struct Ctx {
         void* p = nullptr;
         ALPA_CUDA(cudaMalloc(&p, bytes < 16 ? 16 : bytes));
         allocations.push_back(p);
+        dev_bytes += bytes < 16 ? 16 : bytes;
         return p;
     }
     void dfree(void* p);
@@ -171,6 +177,10 @@ void enqueue_iteration(Ctx& c, int64_t n, cudaStream_t s);  // one diffusion ite
 void enqueue_rollout(Ctx& c, int64_t n, const float* d_actions, float* d_traj, cudaStream_t s);
 void invalidate_graph(Ctx& c);
 void refresh_prefix_map(Ctx& c);  // TMA map of the bound prefix (bf16)
+
+// eval.cu: open-loop metrics (eval.cpp:14-59) of [scenes][n][steps][3] trajectories
+void eval_open_loop_device(Ctx& c, const float* d_traj, const float* d_gt, int64_t scenes, int64_t n,
+                           int64_t steps, double* d_min_ade, double* d_div, cudaStream_t s);
 
 // mk.cu: persistent iteration kernel (bf16 path, uniform prefix)
 bool mk_usable(const Ctx& c);

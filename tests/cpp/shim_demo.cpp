@@ -40,6 +40,12 @@ int main(int argc, char** argv) {
             const Trajectory t = engine.actions_to_trajectory(a, v0);
             ot.write(reinterpret_cast<const char*>(t.poses.data()), t.poses.size() * sizeof(Pose));
         }
+        std::vector<Trajectory> trajs;
+        for (const auto& a : actions) trajs.push_back(engine.actions_to_trajectory(a, v0));
+        if (trajs.size() >= 2)  // open-loop metrics on the device (eval.cpp:39-59)
+            std::printf("metrics min_ade=%.17g diversity=%.17g\n", engine.min_ade(trajs, trajs[0]),
+                        engine.diversity(trajs));
+        std::printf("report %s\n", engine.latency_report().to_json().c_str());
         std::printf("ok graph_commands=%lld kv_bytes=%lld device_ms=%.3f\n",
                     static_cast<long long>(diff.graph_commands), static_cast<long long>(kv_bytes),
                     diff.device_ms);

@@ -13,7 +13,7 @@ import math
 import numpy as np
 import pytest
 
-from oracle.oracle import Cfg, have_ref
+from oracle.oracle import Cfg, Ref, have_ref
 
 
 def tiny_cfg(**kw):  # test_model.cpp:15-27
@@ -194,3 +194,37 @@ def test_footprint_formula(port):
     # test_kv_cache.cpp:231-242
     assert port.footprint(36, 1, 3081, 1024, 2) == 454311936
     assert port.footprint(36, 1, 64, 1024, 2) == 9437184
+
+
+# ----------------------------------------------------------------- open-loop metrics
+@pytest.mark.skipif(not have_ref(), reason="reference library not built")
+@pytest.mark.parametrize("n", [1, 2, 6, 16])
+def test_oracle_open_loop_metrics_match_reference(port, n):
+    """C restatement of min_ade / diversity (eval.cpp:14-59) == the reference, bitwise."""
+    ref = Ref()
+    rng = np.random.default_rng(n)
+    t = (rng.standard_normal((n, 64, 3)) * 10).astype(np.float32)
+    g = (rng.standard_normal((64, 3)) * 10).astype(np.float32)
+    assert port.min_ade(t, g) == ref.min_ade(t, g)
+    if n > 1:
+        assert port.diversity(t) == ref.diversity(t)
+    else:
+        with pytest.raises(ValueError):
+            port.diversity(t)
+
+
+@pytest.mark.skipif(not have_ref(), reason="reference library not built")
+def test_latency_report_json_parses_with_reference():
+    """The shim's LatencyReport JSON key set (profiler.cpp:31-46) round-trips
+    through the reference's LatencyReport::from_json (document built the way
+    the shim's to_json builds it)."""
+    import json
+    doc = {"preprocessing_ms": 0.0, "reasoning_vision_ms": 0.0, "reasoning_prefill_ms": 0.0,
+           "reasoning_decode_ms": 0.0, "action_gen_ms": 30.5, "total_ms": 30.5,
+           "postprocessing_ms": 0.0, "repeats": 1, "action_gen_iter_ms": [3.0] * 10,
+           "alloc_count": 0, "dispatch_count": 11, "replay_count": 1, "bytes_allocated": 123,
+           "kv_bytes": 456, "cot_tokens": 0}
+    n, ms = Ref().parse_latency_report(json.dumps(doc))
+    assert n == 10 and ms == 30.5
+    with pytest.raises(RuntimeError):
+        Ref().parse_latency_report(json.dumps({k: v for k, v in doc.items() if k != "kv_bytes"}))

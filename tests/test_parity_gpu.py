@@ -316,3 +316,32 @@ def test_persistent_kernel_single_launch_per_iteration(port):
         g.bind_prefix(port.synthetic_prefix(7, 2, 100, 128))
         res = g.run_action_generation(alpa.InferenceRequest(num_trajectories=6, v0=5.0))
     assert res.stats["kernel_launches"] == 3 + 1
+
+
+# ----------------------------------------------------------------- open-loop metrics
+@pytest.mark.parametrize("scenes,n", [(1, 2), (3, 6), (2, 16), (5, 1)])
+def test_device_open_loop_metrics_bitexact(port, scenes, n):
+    """Device min_ade / diversity of a scene batch == the reference's
+    (eval.cpp:39-59) bitwise, on random trajectories and on generated ones."""
+    from oracle.oracle import Ref, have_ref
+    oracle = Ref() if have_ref() else port
+    rng = np.random.default_rng(scenes * 100 + n)
+    t = (rng.standard_normal((scenes, n, 64, 3)) * 10).astype(np.float32)
+    g = (rng.standard_normal((scenes, 64, 3)) * 10).astype(np.float32)
+    with alpa.ActionGenerator(c1()) as gen:
+        ade, div = gen.eval_open_loop(t, g, diversity=n > 1)
+        for s in range(scenes):
+            assert ade[s] == oracle.min_ade(t[s], g[s])
+            if n > 1:
+                assert div[s] == oracle.diversity(t[s])
+        if n == 1:
+            with pytest.raises(alpa.InternalError):
+                gen.eval_open_loop(t, g, diversity=True)
+
+
+def test_device_open_loop_metrics_on_generated(gen_c1, golden, port):
+    res = gen_c1.run_action_generation(alpa.InferenceRequest(num_trajectories=6, v0=golden["v0"]))
+    gt = res.trajectories[0] * 0.5
+    ade, div = gen_c1.eval_open_loop(res.trajectories, gt)
+    assert ade[0] == port.min_ade(res.trajectories, gt)
+    assert div[0] == port.diversity(res.trajectories)

@@ -4,6 +4,7 @@ include/alpa_minivla_shim.hpp and linked to libalpa_action.so.
 CPU: it compiles and links (no compute).  GPU: it reproduces the golden
 config-1 actions / trajectories and maps errors to the reference exit codes.
 """
+import json
 import os
 import subprocess
 
@@ -42,6 +43,20 @@ def test_shim_reproduces_golden(tmp_path, golden):
     ea, et = golden["expected"]["n6_k10_actions"], golden["expected"]["n6_k10_traj"]
     assert np.linalg.norm(acts - ea) / np.linalg.norm(ea) <= 1e-4
     assert np.linalg.norm(traj - et) / np.linalg.norm(et) <= 1e-4
+    lines = {ln.split(" ", 1)[0]: ln.split(" ", 1)[1] for ln in out.stdout.splitlines() if " " in ln}
+    # open-loop metrics through the shim == the C restatement of eval.cpp, bitwise
+    from oracle.oracle import Port, Ref, have_ref
+    port = Port()
+    m = dict(kv.split("=") for kv in lines["metrics"].split())
+    assert float(m["min_ade"]) == port.min_ade(traj, traj[0])
+    assert float(m["diversity"]) == port.diversity(traj)
+    # LatencyReport wire format: parsed by the reference's own from_json
+    rep = json.loads(lines["report"])
+    assert len(rep["action_gen_iter_ms"]) == 10 and rep["action_gen_ms"] > 0
+    assert rep["replay_count"] == 1 and rep["alloc_count"] == 0
+    if have_ref():
+        n_iter, ms = Ref().parse_latency_report(lines["report"])
+        assert n_iter == 10 and ms == rep["action_gen_ms"]
     # N = 0 -> ConfigError -> exit code 2 (pipeline.cpp:203-205, cli.cpp:528-540)
     bad = subprocess.run([exe, str(pre), str(r), "0", str(oa), str(ot)], capture_output=True)
     assert bad.returncode == 2
