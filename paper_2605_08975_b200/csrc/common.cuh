@@ -50,21 +50,20 @@ __device__ inline float gelu_fast(float x) {
     return __fdividef(x, 1.0f + ex2f(-2.8853900817779268f * z));
 }
 
-// Same erf fit, as 0.5 x (1 + tanh(z)) with the single-MUFU tanh.approx
-// (|err| <= 5e-4 * |x|, below the bf16 quantum of the GELU output).  The
-// persistent kernel's epilogue is MUFU-bound with the ex2 + rcp form.
+// GELU for the persistent kernel's bf16 epilogues: the tanh form
+// 0.5 x (1 + tanh(sqrt(2/pi) (x + 0.044715 x^3))) with the single-MUFU
+// tanh.approx.  |gelu_tanh - gelu_erf| <= 4.8e-4 (max at |x| ~ 2.7) and
+// <= 1.8e-4 |x|: below the bf16 quantum of the output.  6 instructions: the
+// epilogue is instruction-issue bound (8 warps drain a 128 x TN tile).
 __device__ inline float tanh_approx(float x) {
     float y;
     asm("tanh.approx.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
 __device__ inline float gelu_tanh(float x) {
-    const float u = fminf(fmaxf(x * 0.70710678118654752f, -4.5f), 4.5f);
-    const float u2 = u * u;
-    const float z = u * fmaf(fmaf(fmaf(-1.52990796e-04f, u2, -1.10976167e-03f), u2, 1.03380981e-01f), u2,
-                             1.12828571e+00f);
+    const float u = x * fmaf(0.0356774081f, x * x, 0.7978845608f);
     const float hx = 0.5f * x;
-    return fmaf(hx, tanh_approx(z), hx);
+    return fmaf(hx, tanh_approx(u), hx);
 }
 
 __device__ inline float warp_sum(float v) {
@@ -213,6 +212,27 @@ __device__ inline void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
           "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
         : "r"(taddr));
 }
+// 16 lanes x 256 bit, two 8-column groups (the mma C-fragment layout, measured
+// with tools/tmem_layout.cu): thread t gets (lane t/4, cols 2(t%4), 2(t%4)+1) in
+// r0, r1, (lane t/4 + 8, same cols) in r2, r3; r4..r7 the same for cols + 8.
+__device__ inline void tmem_ld16x256b_x2(uint32_t taddr, uint32_t (&r)[8]) {
+    asm volatile("tcgen05.ld.sync.aligned.16x256b.x2.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                   "=r"(r[6]), "=r"(r[7])
+                 : "r"(taddr));
+}
+// Four 8x8 b16 matrices, stored transposed: thread t's register i holds
+// (row t/4, cols 2(t%4), +1) of matrix i; stored row j of matrix i (= its
+// column j, 16 bytes) goes to the address thread 8i + j supplies.
+__device__ inline void stmatrix_x4_trans(uint32_t saddr, uint32_t r0, uint32_t r1, uint32_t r2, uint32_t r3) {
+    asm volatile("stmatrix.sync.aligned.m8n8.x4.trans.shared.b16 [%0], {%1, %2, %3, %4};" ::"r"(saddr), "r"(r0),
+                 "r"(r1), "r"(r2), "r"(r3)
+                 : "memory");
+}
+__device__ inline uint32_t pack_bf16x2(float lo, float hi) {
+    __nv_bfloat162 b = __floats2bfloat162_rn(lo, hi);
+    return *reinterpret_cast<uint32_t*>(&b);
+}
 __device__ inline void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
@@ -345,6 +365,12 @@ __device__ inline void tma_store_2d(const CUtensorMap* m, const void* src, int c
     asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
                      reinterpret_cast<uint64_t>(m)),
                  "r"(smem_u32(src)), "r"(c0), "r"(c1)
+                 : "memory");
+}
+__device__ inline void tma_store_3d(const CUtensorMap* m, const void* src, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(m)),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
                  : "memory");
 }
 __device__ inline void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }

@@ -91,7 +91,8 @@ struct MkState {
     size_t trace_elems = 0;
     std::vector<const char*> tags;
     std::vector<double> flops;
-    void* fn = nullptr;
+    void* fn = nullptr;     // production kernel
+    void* fn_tr = nullptr;  // instrumented twin (trace / per-op spans)
     int smem = 0, grid = 0;
 };
 
@@ -196,5 +197,7 @@ void make_tmap_bf16_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_
                        uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer);
 void make_tmap_f32_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
                       uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer);
+void make_tmap_f32_3d_sw128(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+                            uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box1);
 
 }  // namespace alpa

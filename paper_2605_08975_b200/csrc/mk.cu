@@ -27,8 +27,9 @@ int num_sms(Ctx& c) {
 }
 
 template <int TN, int HD>
-void* kernel_ptr() {
-    return reinterpret_cast<void*>(mk::iter_kernel<TN, HD>);
+void* kernel_ptr(bool tr) {
+    return tr ? reinterpret_cast<void*>(mk::iter_kernel<TN, HD, true>)
+              : reinterpret_cast<void*>(mk::iter_kernel<TN, HD, false>);
 }
 template <int TN, int HD>
 int kernel_smem() {
@@ -36,12 +37,13 @@ int kernel_smem() {
 }
 
 struct KSel {
-    void* fn;
+    void* fn;     // production kernel
+    void* fn_tr;  // instrumented twin (ALPA_MK_TRACE / alpa_profile spans)
     int smem;
 };
 KSel select_kernel(int tn, int hd) {
 #define ALPA_MK_CASE(T, D) \
-    if (tn == T && hd == D) return {kernel_ptr<T, D>(), kernel_smem<T, D>()};
+    if (tn == T && hd == D) return {kernel_ptr<T, D>(false), kernel_ptr<T, D>(true), kernel_smem<T, D>()};
     ALPA_MK_CASE(64, 64) ALPA_MK_CASE(64, 128) ALPA_MK_CASE(128, 64) ALPA_MK_CASE(128, 128)
     ALPA_MK_CASE(192, 64) ALPA_MK_CASE(192, 128) ALPA_MK_CASE(256, 64) ALPA_MK_CASE(256, 128)
 #undef ALPA_MK_CASE
@@ -178,6 +180,14 @@ void mk_prepare(Ctx& c, int64_t n) {
         // the TMEM layout, tokens split evenly in 16-token halves per warp half)
         const bool splittable = epi == EPI_RESID_F32 || epi == EPI_F32;
         op.splits = splittable ? std::min(cap[kind], pick_splits(tiles, KB, ttn, G)) : 1;
+        // the split finalisation stages its TN/S owned rows (fp32 + bf16 copy) in the
+        // epilogue staging region and runs 4 threads per row: no split where that does not fit
+        while (op.splits > 1) {
+            const int orows = ttn / op.splits;
+            if ((size_t)orows * (512 + 256) <= (size_t)tn * 256 && orows % 16 == 0 && orows <= 64) break;
+            --op.splits;
+            while (op.splits > 1 && ttn % op.splits) --op.splits;
+        }
         op.kbs = (KB + op.splits - 1) / op.splits;
         op.n_items = tiles * op.splits;
         op.split_base = split_ctr;
@@ -190,11 +200,9 @@ void mk_prepare(Ctx& c, int64_t n) {
             // split finalisation: TN/S owned rows, fp32 e + bf16 copy via TMA stores
             const int orows = ttn / op.splits;
             CUtensorMap te{};
-            if ((size_t)orows * (512 + 256) <= (size_t)tn * 256 && orows % 8 == 0) {  // staging fits
             make_tmap_f32_2d(&te, out, (uint64_t)L.out, (uint64_t)M, (uint64_t)ldo * 4, 128, (uint32_t)orows);
             op.tmEs = dm(add_map(te));
             if (produce) op.tmXs = dm(act_map(c.ws.x, ah, orows));
-            }
         }
         op.bias = L.b;
         op.colsum = consume ? L.colsum : nullptr;
@@ -207,7 +215,8 @@ void mk_prepare(Ctx& c, int64_t n) {
         if (consume) op.stats_in = stats;
         op.pf_ptr = pf;
         op.pf_bytes = pfb;
-        if (op.splits > 1) ws_floats = std::max(ws_floats, (size_t)op.splits * M * op.nf);
+        // split partials: [tile][split][TN rows][128 features] fp32 blocks
+        if (op.splits > 1) ws_floats = std::max(ws_floats, (size_t)tiles * op.splits * ttn * 128);
         push(op, tag, 2.0 * M * L.in * L.out);
     };
     const int64_t pre_block = 2 * r * kv * 2;
@@ -225,6 +234,7 @@ void mk_prepare(Ctx& c, int64_t n) {
          "gemm_enc_mlp1", 4);
     gemm(c.mlp2, menc2, c.ws.h1, EPI_F32, c.ws.e, ah, true, false, c.blocks[0].qkv.w, wb(c.blocks[0].qkv),
          "gemm_enc_mlp2", 5);
+    std::vector<std::pair<int, int>> attn_part_maps;  // (map index, splits)
     const int qtiles = (int)((M + 127) / 128);
     const int nbp = (int)((r + 63) / 64);
     for (int64_t b = 0; b < B; ++b) {
@@ -252,6 +262,14 @@ void mk_prepare(Ctx& c, int64_t n) {
             op.pre_v_row = (blkrow + 1) * r;
             op.pf_ptr = blk.o.w;
             op.pf_bytes = wb(blk.o);
+            if (op.splits > 1) {
+                // partial staging reuses the Q/P smem: one item per CTA (a next item's Q
+                // load could otherwise land on it)
+                if (op.n_items > G) fail(ALPA_ERR_INTERNAL, "persistent kernel: attention split plan exceeds one wave");
+                const int mp = add_map(CUtensorMap{});  // encoded once the workspace exists
+                attn_part_maps.push_back({mp, op.splits});
+                op.tmXs = dm(mp);
+            }
             ws_floats = std::max(ws_floats, (size_t)op.splits * M * kv);
             wsml_elems = std::max(wsml_elems, (size_t)op.splits * M * H);
             push(op, "attention", 4.0 * n * A * (r + A) * kv);
@@ -271,6 +289,11 @@ void mk_prepare(Ctx& c, int64_t n) {
         push(op, "head_update", 4.0 * M * ah + 8.0 * M);
     }
 
+    m.ws = (float*)c.dalloc(ws_floats * sizeof(float));
+    m.wsml = (float2*)c.dalloc(wsml_elems * sizeof(float2));
+    for (auto& pm : attn_part_maps)
+        make_tmap_f32_3d_sw128(&maps[pm.first], m.ws, (uint64_t)kv, (uint64_t)M, (uint64_t)pm.second,
+                               (uint64_t)kv * 4, (uint64_t)M * kv * 4, 128);
     m.d_maps = (CUtensorMap*)c.dalloc(maps.size() * sizeof(CUtensorMap));
     ALPA_CUDA(cudaMemcpy(m.d_maps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
     auto fix = [&](const CUtensorMap*& t) {
@@ -298,19 +321,19 @@ void mk_prepare(Ctx& c, int64_t n) {
                         ops[o].n_items, ops[o].splits, ops[o].tn, ops[o].dep, ops[o].dep_count);
     }
     ALPA_CUDA(cudaMemset(m.d_counters, 0, m.counter_ints * sizeof(int)));
-    m.ws = (float*)c.dalloc(ws_floats * sizeof(float));
-    m.wsml = (float2*)c.dalloc(wsml_elems * sizeof(float2));
     m.d_tstamp = (unsigned long long*)c.dalloc((m.n_ops + 1) * sizeof(unsigned long long));
     if (const char* e = getenv("ALPA_MK_TRACE"); e && e[0] == '1') {
-        m.trace_elems = (size_t)m.n_ops * G * 16;
+        m.trace_elems = (size_t)m.n_ops * G * mk::TR_NSLOT;
         m.d_trace = (unsigned long long*)c.dalloc(m.trace_elems * sizeof(unsigned long long));
     }
     m.tags = tags;
     m.flops = flops;
     m.fn = ks.fn;
+    m.fn_tr = ks.fn_tr;
     m.smem = ks.smem;
     m.grid = G;
     ALPA_CUDA(cudaFuncSetAttribute(ks.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, ks.smem));
+    ALPA_CUDA(cudaFuncSetAttribute(ks.fn_tr, cudaFuncAttributeMaxDynamicSharedMemorySize, ks.smem));
     int occ = 0;
     ALPA_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, ks.fn, mk::Cfg<64, 64>::THREADS, ks.smem));
     if (occ < 1) fail(ALPA_ERR_INTERNAL, "persistent kernel does not fit on an SM");
@@ -364,7 +387,7 @@ void mk_enqueue(Ctx& c, int64_t n, cudaStream_t s, unsigned long long* tstamp,
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     void* args[] = {&p};
-    ALPA_CUDA(cudaLaunchKernelExC(&cfg, m.fn, args));
+    ALPA_CUDA(cudaLaunchKernelExC(&cfg, (tstamp || trace) ? m.fn_tr : m.fn, args));
     c.last_launches++;
 }
 

@@ -61,6 +61,7 @@ struct Op {
     const CUtensorMap* tmXB; // GEMM, unsplit residual producer: bf16 copy map, box {64,TN}
     const CUtensorMap* tmEs; // GEMM, split residual producer: fp32 rows, box {128, TN/S}
     const CUtensorMap* tmXs; // GEMM, split residual producer: bf16 copy, box {64, TN/S}
+                             // attention: fp32 KV-split partials [S][M][kv], box {32, 128, 1} SW128
     const float* bias;
     const float* colsum;     // LN-folded consumers
     void* out;
@@ -111,6 +112,16 @@ enum TraceEv : int {
     TR_BAR = 11,     // epilogue warp 2: staging barrier passed
     TR_ACC9 = 12,    // epilogue warp 9: accumulator ready
     TR_LOOP9 = 13,   // epilogue warp 9: drain loop done
+    TR_FIXC0 = 16,   // split finalisation: chunk 0, 1, 2 of fix_t done (16..18)
+    TR_FIXED = 19,   // split finalisation: fix_t returned
+    TR_STORE = 20,   // split finalisation: staging fenced, TMA stores issued
+    TR_STATS = 21,   // split finalisation: row statistics written
+    TR_MERGE = 22,   // attention: key-half merge + partial stores done
+    TR_FIXIN = 23,   // split finalisation: fix_t entered (slot 7 of FixArgs::tr)
+    TR_FIXV0 = 24,   // split finalisation: chunk 0 values computed (slot 8)
+    TR_SM0 = 25,     // attention: first S block ready (softmax starts)
+    TR_SMX = 26,     // attention: softmax loop done
+    TR_NSLOT = 32,
 };
 
 template <int TN, int HD>
@@ -193,19 +204,23 @@ __device__ __noinline__ void wait_count(const int* ctr, int want) {
     (void)ld_acquire(ctr);
 }
 
+// Instrumentation (TR kernels only: the production kernel carries none of this
+// code -- the kernel does not fit the instruction cache, every byte counts).
+template <bool TR>
 __device__ inline void stamp(const Params& p, int o) {
-    if (p.tstamp) {
+    if (TR && p.tstamp) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         atomicMax(p.tstamp + o, t);
     }
 }
 
+template <bool TR>
 __device__ inline void trace_ev(const Params& p, int o, int ev) {
-    if (p.trace) {
+    if (TR && p.trace) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        p.trace[((size_t)o * gridDim.x + blockIdx.x) * 16 + ev] = t;
+        p.trace[((size_t)o * gridDim.x + blockIdx.x) * TR_NSLOT + ev] = t;
     }
 }
 
@@ -286,34 +301,46 @@ __device__ inline uint2 pack_bf16x4(float4 v) {
     return pk;
 }
 
-// Merge the 2S attention partials (S KV splits x 2 key halves) of rows
-// [rb, re) of one (head, query tile): log-sum-exp weights, fixed order.
+// Merge the S KV-split partials of rows [rb, re) of one (head, query tile):
+// log-sum-exp weights, fixed split order.  Flat (row, 4-dim group) items, two
+// per thread per pass, every partial load of a pass in flight at once.
 template <int HD>
-__device__ inline void attn_fixup(const Params& p, const Op& op, const AttnItem& a, int rb, int re,
-                                  int ew, int lane) {
-    const int np = op.splits;  // one (already half-merged) partial per KV split
-    const int d = lane * 4;
-    for (int t = rb + ew; t < re; t += 8) {
-        float2 ml[6];
-        float4 v[6];
+__device__ inline void attn_fixup(const Params& p, const Op& op, const AttnItem& a, int rb, int re, int et) {
+    const int np = op.splits;
+    constexpr int NQ = HD / 4;  // 4-dim groups per row
+    const int items = (re - rb) * NQ;
+#pragma unroll 1
+    for (int base = 0; base < items; base += 512) {
+        float2 ml[2][6];
+        float4 v[2][6];
 #pragma unroll
-        for (int q = 0; q < 6; ++q) {
-            ml[q] = q < np ? __ldcg(p.wsml + ((int64_t)q * p.M + t) * p.H + a.h) : make_float2(-INFINITY, 0.f);
-            v[q] = (q < np && d < HD) ? ldcg4(p.ws + ((int64_t)q * p.M + t) * p.kv + a.h * HD + d)
-                                      : make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int k = 0; k < 2; ++k) {
+            const int idx = base + et + k * 256;
+            const bool ok = idx < items;
+            const int t = rb + idx / NQ, d = (idx % NQ) * 4;
+#pragma unroll
+            for (int q = 0; q < 6; ++q) {
+                const bool on = ok && q < np;
+                ml[k][q] = on ? __ldcg(p.wsml + ((int64_t)q * p.M + t) * p.H + a.h) : make_float2(-INFINITY, 0.f);
+                v[k][q] = on ? ldcg4(p.ws + ((int64_t)q * p.M + t) * p.kv + a.h * HD + d) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
         }
-        float mx = -INFINITY;
 #pragma unroll
-        for (int q = 0; q < 6; ++q) mx = fmaxf(mx, ml[q].x);
-        float L = 0.f;
-        float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int k = 0; k < 2; ++k) {
+            const int idx = base + et + k * 256;
+            if (idx >= items) continue;
+            const int t = rb + idx / NQ, d = (idx % NQ) * 4;
+            float mx = -INFINITY;
 #pragma unroll
-        for (int q = 0; q < 6; ++q) {
-            const float w = ml[q].x == -INFINITY ? 0.f : ex2(ml[q].x - mx);
-            L += w * ml[q].y;
-            o.x += w * v[q].x; o.y += w * v[q].y; o.z += w * v[q].z; o.w += w * v[q].w;
-        }
-        if (d < HD) {
+            for (int q = 0; q < 6; ++q) mx = fmaxf(mx, ml[k][q].x);
+            float L = 0.f;
+            float4 o = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int q = 0; q < 6; ++q) {
+                const float w = ml[k][q].x == -INFINITY ? 0.f : ex2(ml[k][q].x - mx);
+                L += w * ml[k][q].y;
+                o.x += w * v[k][q].x; o.y += w * v[k][q].y; o.z += w * v[k][q].z; o.w += w * v[k][q].w;
+            }
             const float inv = 1.0f / L;
             *reinterpret_cast<uint2*>(reinterpret_cast<__nv_bfloat16*>(op.out) + (int64_t)t * p.kv + a.h * HD + d) =
                 pack_bf16x4(make_float4(o.x * inv, o.y * inv, o.z * inv, o.w * inv));
@@ -331,236 +358,245 @@ __device__ inline void sts_bf16_t(uint8_t* base, int row, int fl, float v) {
 }
 #define sts_bf16(base, row, fl, v) sts_bf16_t<TN>(base, row, fl, v)
 
-// Generic drain of one thread's accumulator row (feature fl, ncol tokens from
-// column c0 of the tile) for every unsplit GEMM epilogue.  ONE out-of-line copy
-// serves all ops, so its code stays in the instruction cache across ops (a
-// persistent kernel's per-op specialised epilogues were each cold on every use).
-// Element math is branch-free; every optional step is a per-group uniform branch.
+// Drain of an unsplit GEMM accumulator (every bf16 / fp32 epilogue kind).
+// TMEM is read in the 16x256b shape (the mma C-fragment layout): per 16-token
+// chunk a thread holds 4 features (fa + 8k) x 4 tokens, so the bf16 tile goes
+// to the SW128 staging with one stmatrix.trans per 8 tokens (16-byte rows, no
+// per-element addressing) and the per-token row statistics need only a 3-round
+// butterfly.  Straight-line per epilogue kind (uniform choices hoisted: a
+// per-element branch serialises every element's dependency chain).
 //   v = rs*(acc - mu*cs) + b   (mu = 0, rs = 1 without LayerNorm: exact)
-//   v = e + v                  (staged residual; 0 otherwise)
-//   GELU; f32 store; bf16 into the TMA-store staging; row statistics.
+//   v = e + v                  (staged residual in TMEM columns 256+)
+//   GELU; fp32 store; bf16 staging; row statistics.
 struct DrainArgs {
-    uint32_t tacc, testage;  // TMEM: accumulator, staged residual (~0: none)
-    int ncol, c0, fl, q, lane, gelu;
-    float bf, cs;
-    const float* mu_s;       // LayerNorm (mu, rstd) per token or null
+    uint32_t tacc, tres;     // TMEM of the warp's lane quarter at the half's first token (acc / residual)
+    int ncol;                // tokens of this warp half, multiple of 16
+    int nvalid;              // of which inside M
+    int cb;                  // first token of the half (tile-local)
+    int q, lane;
+    float bf[4], cs[4];      // per feature fa + 8k
+    const float* mu_s;       // LayerNorm (mu, rstd) per tile token
     const float* rs_s;
-    float* erow;             // f32 output at token c0 (stride ldo) or null
+    float* eout;             // fp32 output at (tile token 0, feature fa) (row stride ldo) or null
     long long ldo;
-    uint8_t* stg;            // bf16 staging image or null
-    int stg_panel;           // bytes between the two 64-feature panels
+    uint8_t* stg;            // bf16 staging (two SW128 panels of [TN][128 B]) or null
+    int tn;
     float2* st_part;         // row-stat partials [4][256] or null
-    float* part;             // split-K partial row at token c0 (stride ldo): only this
-    int dbg;                 // microbenchmarks only: 1 = no TMEM loads
 };
-template <bool LN, bool GELU, bool RESID, bool F32, bool STG, bool PART>
+template <bool LN, bool GELU, bool RESID, bool F32, bool STATS>
 __device__ __forceinline__ void drain_t(const DrainArgs& a) {
-    const int col = a.fl & 63;
-    uint8_t* sbase = STG ? a.stg + (a.fl >> 6) * a.stg_panel + (col & 7) * 2 : nullptr;
+    const int tq = a.lane & 3, tr = a.lane >> 2;
+    // stmatrix row addresses: matrix i = lane >> 3 (features 8i..), row j = lane & 7 (token)
+    const int mj = a.lane & 7;
+    const int chunk = (a.q & 1) * 4 + (a.lane >> 3);
+    const uint32_t sbase = a.stg ? smem_u32(a.stg) + (a.q >> 1) * (a.tn * 128) : 0u;
 #pragma unroll 1
-    for (int c = 0; c < a.ncol; c += 8) {
-        uint32_t r[8], rv[8];
-        if (a.dbg & 1) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) r[j] = rv[j] = __float_as_uint((float)(c + j));
-        } else {
-            tmem_ld8(a.tacc + c, r);
-            if constexpr (RESID) tmem_ld8(a.testage + c, rv);
-            tmem_ld_wait();
+    for (int c = 0; c < a.ncol; c += 16) {
+        uint32_t A[8], B[8], RA[8], RB[8];
+        tmem_ld16x256b_x2(a.tacc + c, A);
+        tmem_ld16x256b_x2(a.tacc + (16u << 16) + c, B);
+        if constexpr (RESID) {
+            tmem_ld16x256b_x2(a.tres + c, RA);
+            tmem_ld16x256b_x2(a.tres + (16u << 16) + c, RB);
         }
-        if constexpr (PART) {
-            float* d = a.part + (long long)c * a.ldo;
+        tmem_ld_wait();
+        // v[k][m]: feature fa + 8k, token t_m = cb + c + (m >> 1) * 8 + 2 tq + (m & 1)
+        float v[4][4];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) stg(d + j * a.ldo, __uint_as_float(r[j]));
-        } else {
-            float v[8];
-            float mu[8], rs[8];
-            if constexpr (LN) {
-                *reinterpret_cast<float4*>(mu) = *reinterpret_cast<const float4*>(a.mu_s + a.c0 + c);
-                *reinterpret_cast<float4*>(mu + 4) = *reinterpret_cast<const float4*>(a.mu_s + a.c0 + c + 4);
-                *reinterpret_cast<float4*>(rs) = *reinterpret_cast<const float4*>(a.rs_s + a.c0 + c);
-                *reinterpret_cast<float4*>(rs + 4) = *reinterpret_cast<const float4*>(a.rs_s + a.c0 + c + 4);
-            }
+        for (int m = 0; m < 4; ++m) {
+            const int ri = (m >> 1) * 4 + (m & 1);
+            v[0][m] = __uint_as_float(A[ri]);
+            v[1][m] = __uint_as_float(A[ri + 2]);
+            v[2][m] = __uint_as_float(B[ri]);
+            v[3][m] = __uint_as_float(B[ri + 2]);
+        }
+        float mu[4], rs[4];
+        if constexpr (LN) {
+            const int t0 = a.cb + c + 2 * tq;
+            const float2 m0 = *reinterpret_cast<const float2*>(a.mu_s + t0);
+            const float2 m1 = *reinterpret_cast<const float2*>(a.mu_s + t0 + 8);
+            const float2 r0 = *reinterpret_cast<const float2*>(a.rs_s + t0);
+            const float2 r1 = *reinterpret_cast<const float2*>(a.rs_s + t0 + 8);
+            mu[0] = m0.x; mu[1] = m0.y; mu[2] = m1.x; mu[3] = m1.y;
+            rs[0] = r0.x; rs[1] = r0.y; rs[2] = r1.x; rs[3] = r1.y;
+        }
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const float acc = __uint_as_float(r[j]);
-                float x = LN ? rs[j] * (acc - mu[j] * a.cs) + a.bf : acc + a.bf;
-                if constexpr (RESID) x = __uint_as_float(rv[j]) + x;
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+                float x = LN ? rs[m] * (v[k][m] - mu[m] * a.cs[k]) + a.bf[k] : v[k][m] + a.bf[k];
+                if constexpr (RESID) {
+                    const int ri = (m >> 1) * 4 + (m & 1) + (k & 1) * 2;
+                    x = __uint_as_float(k < 2 ? RA[ri] : RB[ri]) + x;
+                }
                 if constexpr (GELU) x = gelu_tanh(x);
-                v[j] = x;
+                v[k][m] = x;
             }
-            if constexpr (F32) {
-                float* d = a.erow + (long long)c * a.ldo;
+        if constexpr (F32) {
 #pragma unroll
-                for (int j = 0; j < 8; ++j) stg(d + j * a.ldo, v[j]);
-            }
-            if constexpr (STG) {
-                if (!(a.dbg & 2)) {
+            for (int m = 0; m < 4; ++m) {
+                const int tl = c + (m >> 1) * 8 + 2 * tq + (m & 1);  // token within the half
+                if (tl < a.nvalid) {
+                    float* d = a.eout + (long long)(a.cb + tl) * a.ldo + tr;
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        const int row = a.c0 + c + j;
-                        *reinterpret_cast<__nv_bfloat16*>(sbase + row * 128 + ((((col >> 3) ^ (row & 7))) << 4)) =
-                            __float2bfloat16_rn(v[j]);
-                    }
+                    for (int k = 0; k < 4; ++k) stg(d + 8 * k, v[k][m]);
                 }
             }
-            if constexpr (F32) {
-                if (a.st_part) {
-                    // transpose-reduce: 8 token sums over the warp's 32 features;
-                    // lane ends with token (lane >> 2) & 7
-                    float a1[8], a2[8];
+        }
+        if (a.stg) {
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) { a1[j] = v[j]; a2[j] = v[j] * v[j]; }
+            for (int g = 0; g < 2; ++g) {
+                const int tok = a.cb + c + g * 8 + mj;
+                stmatrix_x4_trans(sbase + tok * 128 + ((chunk ^ (tok & 7)) << 4),
+                                  pack_bf16x2(v[0][2 * g], v[0][2 * g + 1]), pack_bf16x2(v[1][2 * g], v[1][2 * g + 1]),
+                                  pack_bf16x2(v[2][2 * g], v[2][2 * g + 1]), pack_bf16x2(v[3][2 * g], v[3][2 * g + 1]));
+            }
+        }
+        if constexpr (STATS) {
+            // per token: sum over the thread's 4 features, then over the 8 lanes
+            // sharing tq (xor 4, 8, 16): fixed order, deterministic
+            float s1[4], s2[4];
 #pragma unroll
-                    for (int rr = 0; rr < 3; ++rr) {
-                        const int off = 16 >> rr, half = 4 >> rr;
-                        const bool up = (a.lane & off) != 0;
+            for (int m = 0; m < 4; ++m) {
+                s1[m] = (v[0][m] + v[1][m]) + (v[2][m] + v[3][m]);
+                s2[m] = (v[0][m] * v[0][m] + v[1][m] * v[1][m]) + (v[2][m] * v[2][m] + v[3][m] * v[3][m]);
+            }
 #pragma unroll
-                        for (int i2 = 0; i2 < half; ++i2) {
-                            const float s1 = up ? a1[i2] : a1[i2 + half];
-                            const float s2 = up ? a2[i2] : a2[i2 + half];
-                            const float k1 = up ? a1[i2 + half] : a1[i2];
-                            const float k2 = up ? a2[i2 + half] : a2[i2];
-                            a1[i2] = k1 + __shfl_xor_sync(0xffffffffu, s1, off);
-                            a2[i2] = k2 + __shfl_xor_sync(0xffffffffu, s2, off);
-                        }
-                    }
-                    a1[0] += __shfl_xor_sync(0xffffffffu, a1[0], 2);
-                    a2[0] += __shfl_xor_sync(0xffffffffu, a2[0], 2);
-                    a1[0] += __shfl_xor_sync(0xffffffffu, a1[0], 1);
-                    a2[0] += __shfl_xor_sync(0xffffffffu, a2[0], 1);
-                    if ((a.lane & 3) == 0)
-                        a.st_part[a.q * 256 + a.c0 + c + ((a.lane >> 2) & 7)] = make_float2(a1[0], a2[0]);
+            for (int off = 4; off < 32; off <<= 1)
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    s1[m] += __shfl_xor_sync(0xffffffffu, s1[m], off);
+                    s2[m] += __shfl_xor_sync(0xffffffffu, s2[m], off);
                 }
+            if (tr == 0) {
+#pragma unroll
+                for (int m = 0; m < 4; ++m)
+                    a.st_part[a.q * 256 + a.cb + c + (m >> 1) * 8 + 2 * tq + (m & 1)] = make_float2(s1[m], s2[m]);
             }
         }
     }
 }
 
-// Split-K finalisation of one thread's owned tokens (TMEM layout): the own
-// split's partial is read from TMEM, the others' from the L2 workspace, summed
-// in split order 0..S-1 (deterministic), + bias (+ staged residual).
+// Mode dispatch (each epilogue kind has its own straight-line instance).
+__device__ inline void drain(const DrainArgs& a, bool ln, bool gelu, bool resid, bool f32, bool stats) {
+    if (resid) drain_t<false, false, true, true, true>(a);
+    else if (f32 && stats) drain_t<false, false, false, true, true>(a);
+    else if (f32) drain_t<false, false, false, true, false>(a);
+    else if (ln && gelu) drain_t<true, true, false, false, false>(a);
+    else if (ln) drain_t<true, false, false, false, false>(a);
+    else if (gelu) drain_t<false, true, false, false, false>(a);
+    else drain_t<false, false, false, false, false>(a);
+}
+
+// Split-K finalisation of one thread's owned tokens (TMEM layout): own partial
+// (TMEM) + the other splits' partials (L2 workspace, [tile][split][TN][128]
+// fp32 blocks: constant 512 B row stride, so every load is base + immediate)
+// in a FIXED order (own, then the others by split index: deterministic, graph
+// == eager bitwise) + bias (+ staged residual) -> fp32 staging rows.
 struct FixArgs {
-    uint32_t tacc, testage;
-    int ncol, c0, S, s_own, nf, q, lane;
-    const float* ws;          // workspace at (split 0, first owned token, feature)
-    long long split_stride;   // floats between splits
+    uint32_t tacc, testage;   // TMEM: own partial / staged residual at the first owned token
+    int ncol;                 // owned tokens of this thread, multiple of 8
+    const float* oth[3];      // other splits' partial rows at (first owned token, feature), null: none
     float bf;
-    float* erow;              // direct stores (staging does not fit): f32 output at the first owned token
-    __nv_bfloat16* xrow;      //   and its bf16 copy (or null)
-    long long ldo;
-    float* e_stg;             // fp32 staging [rows][128] (TMA store of the e rows), null: direct stores
-    uint8_t* x_stg;           // bf16 staging, SW128 panels of [rows][64] (null: no copy)
-    int rows;                 // owned rows of the tile (staging row count)
-    int r0;                   // this thread's first staging row
-    float2* st_part;
+    float* e_stg;             // fp32 staging at (first owned row of this thread, feature), row stride 128
+    unsigned long long* tr;   // diagnostics: per-chunk completion times (et 0 only) or null
 };
-template <bool RESID>
+__device__ inline void tr_now(unsigned long long* p) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    *p = t;
+}
+template <bool RESID, bool TR>
 __device__ __forceinline__ void fix_t(const FixArgs& a) {
+    if (TR && a.tr) tr_now(a.tr + 7);
+    const float* o0 = a.oth[0];
+    const float* o1 = a.oth[1];
+    const float* o2 = a.oth[2];
+    float* d = a.e_stg;
 #pragma unroll 1
     for (int c = 0; c < a.ncol; c += 8) {
-        float pv[4][8];
+        float p0[8], p1[8], p2[8];
 #pragma unroll
-        for (int s2 = 0; s2 < 4; ++s2)
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-                pv[s2][j] = (s2 < a.S && s2 != a.s_own) ? __ldcg(a.ws + s2 * a.split_stride + (long long)(c + j) * a.nf) : 0.f;
+        for (int j = 0; j < 8; ++j) {
+            p0[j] = o0 ? __ldcg(o0 + (c + j) * 128) : 0.f;
+            p1[j] = o1 ? __ldcg(o1 + (c + j) * 128) : 0.f;
+            p2[j] = o2 ? __ldcg(o2 + (c + j) * 128) : 0.f;
+        }
         uint32_t r[8], rv[8];
         tmem_ld8(a.tacc + c, r);
         if constexpr (RESID) tmem_ld8(a.testage + c, rv);
         tmem_ld_wait();
-        float v[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            float acc = 0.f;
-#pragma unroll
-            for (int s2 = 0; s2 < 4; ++s2)  // fixed split order 0..S-1
-                if (s2 < a.S) acc += (s2 == a.s_own) ? __uint_as_float(r[j]) : pv[s2][j];
+            float acc = __uint_as_float(r[j]);
+            if (o0) acc += p0[j];
+            if (o1) acc += p1[j];
+            if (o2) acc += p2[j];
             float x = acc + a.bf;
             if constexpr (RESID) x = __uint_as_float(rv[j]) + x;
-            v[j] = x;
+            d[(c + j) * 128] = x;
         }
-        const int fl = a.q * 32 + a.lane;
-        if (!a.e_stg) {
-            float* d = a.erow + (long long)c * a.ldo;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) stg(d + j * a.ldo, v[j]);
-            if (a.xrow) {
-#pragma unroll
-                for (int j = 0; j < 8; ++j) stg(a.xrow + (long long)(c + j) * a.ldo, v[j]);
-            }
-        } else {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) a.e_stg[(a.r0 + c + j) * 128 + fl] = v[j];
-        }
-        if (a.e_stg && a.x_stg) {
-            const int col = fl & 63;
-            uint8_t* xb = a.x_stg + (fl >> 6) * (a.rows * 128) + (col & 7) * 2;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const int row = a.r0 + c + j;
-                *reinterpret_cast<__nv_bfloat16*>(xb + row * 128 + ((((col >> 3) ^ (row & 7))) << 4)) =
-                    __float2bfloat16_rn(v[j]);
-            }
-        }
-        if (a.st_part) {
-            float a1[8], a2[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) { a1[j] = v[j]; a2[j] = v[j] * v[j]; }
-#pragma unroll
-            for (int rr = 0; rr < 3; ++rr) {
-                const int off = 16 >> rr, half = 4 >> rr;
-                const bool up = (a.lane & off) != 0;
-#pragma unroll
-                for (int i2 = 0; i2 < half; ++i2) {
-                    const float s1 = up ? a1[i2] : a1[i2 + half];
-                    const float s2v = up ? a2[i2] : a2[i2 + half];
-                    const float k1 = up ? a1[i2 + half] : a1[i2];
-                    const float k2 = up ? a2[i2 + half] : a2[i2];
-                    a1[i2] = k1 + __shfl_xor_sync(0xffffffffu, s1, off);
-                    a2[i2] = k2 + __shfl_xor_sync(0xffffffffu, s2v, off);
-                }
-            }
-            a1[0] += __shfl_xor_sync(0xffffffffu, a1[0], 2);
-            a2[0] += __shfl_xor_sync(0xffffffffu, a2[0], 2);
-            a1[0] += __shfl_xor_sync(0xffffffffu, a1[0], 1);
-            a2[0] += __shfl_xor_sync(0xffffffffu, a2[0], 1);
-            if ((a.lane & 3) == 0) a.st_part[a.q * 256 + a.c0 + c + ((a.lane >> 2) & 7)] = make_float2(a1[0], a2[0]);
-        }
+        if (TR && a.tr && c < 24) tr_now(a.tr + c / 8);
     }
 }
 
-// Mode dispatch (each op kind has its own straight-line instance).
-__device__ inline void drain(const DrainArgs& a, bool ln, bool gelu, bool resid, bool f32, bool part) {
-    if (part) drain_t<false, false, false, false, false, true>(a);
-    else if (resid) drain_t<false, false, true, true, true, false>(a);
-    else if (f32) drain_t<false, false, false, true, true, false>(a);
-    else if (ln && gelu) drain_t<true, true, false, false, true, false>(a);
-    else if (ln) drain_t<true, false, false, false, true, false>(a);
-    else if (gelu) drain_t<false, true, false, false, true, false>(a);
-    else drain_t<false, false, false, false, true, false>(a);
+// Row pass over the fp32 staging rows of a split finalisation: (sum, sumsq)
+// per row of the 128-feature tile (LayerNorm statistics of the consumer, fixed
+// order) and the bf16 copy into the SW128 staging of a TMA store box {64, rows}.
+// 4 threads per row; step m: thread p takes features [8(4m+p), 8(4m+p)+8), so a
+// row's 4 threads read 128 contiguous bytes; odd rows read the two halves in
+// the other order (the 8 threads of one LDS.128 phase hit 32 distinct banks).
+__device__ inline void fix_rows(const float* e_stg, uint8_t* x_stg, int rows, int n_valid, float2* stats_row0,
+                                int nft, int et) {
+    const int row = et >> 2, part = et & 3;
+    if (row >= rows) return;  // whole 4-thread groups: the shuffles stay converged
+    const float* rp = e_stg + row * 128;
+    const int h = (row & 1) * 4;
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        const int c16 = m * 4 + part;  // 8-feature chunk of the tile
+        const float4 a = *reinterpret_cast<const float4*>(rp + c16 * 8 + h);
+        const float4 b = *reinterpret_cast<const float4*>(rp + c16 * 8 + (4 - h));
+        const float4 u = h ? b : a, w = h ? a : b;
+        s1 += ((u.x + u.y) + (u.z + u.w)) + ((w.x + w.y) + (w.z + w.w));
+        s2 += ((u.x * u.x + u.y * u.y) + (u.z * u.z + u.w * u.w)) + ((w.x * w.x + w.y * w.y) + (w.z * w.z + w.w * w.w));
+        if (x_stg) {
+            const uint2 lo = pack_bf16x4(u), hi = pack_bf16x4(w);
+            *reinterpret_cast<uint4*>(x_stg + (c16 >> 3) * (rows * 128) + row * 128 + (((c16 & 7) ^ (row & 7)) << 4)) =
+                make_uint4(lo.x, lo.y, hi.x, hi.y);
+        }
+    }
+    const unsigned grp = 0xfu << (threadIdx.x & 28);
+    s1 += __shfl_xor_sync(grp, s1, 1);
+    s2 += __shfl_xor_sync(grp, s2, 1);
+    s1 += __shfl_xor_sync(grp, s1, 2);
+    s2 += __shfl_xor_sync(grp, s2, 2);
+    if (stats_row0 && part == 0 && row < n_valid) stats_row0[(int64_t)row * nft] = make_float2(s1, s2);
 }
 
 // Item outputs are complete: make them visible to later generic and TMA
 // (async-proxy) readers, then count the item.
+template <bool TR>
 __device__ inline void publish(const Params& p, int o, int et) {
     if (et == 0) {
-        trace_ev(p, o, TR_FIX);
+        trace_ev<TR>(p, o, TR_FIX);
         bulk_wait_all();  // this item's TMA stores have landed
     }
     fence_proxy_async_global();
     epi_bar();
     if (et == 0) {
-        trace_ev(p, o, TR_FENCE);
+        trace_ev<TR>(p, o, TR_FENCE);
         red_release_add(p.done + o, 1);  // release is cumulative over the CTA's writes (bar.sync)
-        stamp(p, o);
-        trace_ev(p, o, TR_PUB);
+        stamp<TR>(p, o);
+        trace_ev<TR>(p, o, TR_PUB);
     }
 }
 
 // Split rendezvous: every split of a tile has written its partial.  Thread 0
 // also acquires the op's input dependency, so the fixup may read rows other
 // CTAs produced (residual stream, LayerNorm statistics).
+template <bool TR>
 __device__ inline void split_meet(const Params& p, const Op& op, int o, int* ctr, int et) {
     const int S = op.splits;
     epi_bar();
@@ -570,11 +606,11 @@ __device__ inline void split_meet(const Params& p, const Op& op, int o, int* ctr
         wait_count(ctr, S);
     }
     epi_bar();
-    if (et == 0) trace_ev(p, o, TR_MEET);
+    if (et == 0) trace_ev<TR>(p, o, TR_MEET);
 }
 
 // ------------------------------------------------------------------ the kernel
-template <int TN, int HD>
+template <int TN, int HD, bool TR>
 __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Params p) {
     using C = Cfg<TN, HD>;
     extern __shared__ uint8_t smem_raw[];
@@ -597,7 +633,7 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        if (p.tstamp) {
+        if (TR && p.tstamp) {
             unsigned long long t;
             asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
             atomicMin(p.tstamp + p.n_ops, t);
@@ -661,13 +697,13 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                             mbar_expect_tx(&full[st], stage_tx);
                             tma_load_2d_hint(sb, op.tmW, &full[st], (g.kb0 + i) * 64, g.f0, wpol);
                         }
-                        trace_ev(p, o, TR_PRE);
+                        trace_ev<TR>(p, o, TR_PRE);
                         if (!waited && op.dep >= 0) {
                             wait_count(p.done + op.dep, op.dep_count);
                             fence_proxy_async_global();
                             waited = true;
                         }
-                        trace_ev(p, o, TR_DEP);
+                        trace_ev<TR>(p, o, TR_DEP);
                         for (int i = 0; i < g.nkb; ++i) {
                             const uint32_t st = (ks + i) % C::STAGES;
                             uint8_t* sb = smem + st * C::SLOT;
@@ -710,13 +746,13 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                         };
                         int pre = 0;
                         while (pre < a.nj && pre < C::STAGES && a.g0 + pre < op.nbp) load_block(pre++);
-                        trace_ev(p, o, TR_PRE);
+                        trace_ev<TR>(p, o, TR_PRE);
                         if (!waited && op.dep >= 0) {
                             wait_count(p.done + op.dep, op.dep_count);
                             fence_proxy_async_global();
                             waited = true;
                         }
-                        trace_ev(p, o, TR_DEP);
+                        trace_ev<TR>(p, o, TR_DEP);
                         if (natt > 0) mbar_wait(q_empty, (natt - 1) & 1);
                         mbar_expect_tx(q_full, C::Q_BYTES);
                         for (int pn = 0; pn < HD / 64; ++pn)
@@ -746,7 +782,7 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                         for (int i = 0; i < g.nkb; ++i) {
                             const uint32_t st = (ks + i) % C::STAGES, ph = ((ks + i) / C::STAGES) & 1;
                             mbar_wait(&full[st], ph);
-                            if (i == 0) trace_ev(p, o, TR_MMA0);
+                            if (i == 0) trace_ev<TR>(p, o, TR_MMA0);
                             tc_fence_after();
                             uint8_t* sb = smem + st * C::SLOT;
                             const uint64_t da = sdesc_k_sw128(sb);
@@ -757,7 +793,7 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                             tc_commit(&empty[st]);
                         }
                         tc_commit(acc_full);
-                        trace_ev(p, o, TR_MMA1);
+                        trace_ev<TR>(p, o, TR_MMA1);
                         ks += g.nkb;
                         ++nmma;
                     }
@@ -791,7 +827,7 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                             const uint32_t JJ = J + j;
                             const uint32_t st = (ks + j) % C::STAGES, ph = ((ks + j) / C::STAGES) & 1;
                             mbar_wait(&full[st], ph);
-                            if (j == 0) trace_ev(p, o, TR_MMA0);
+                            if (j == 0) trace_ev<TR>(p, o, TR_MMA0);
                             if (JJ >= 2) mbar_wait(&s_free[JJ & 1], ((JJ - 2) >> 1) & 1);
                             tc_fence_after();
                             const uint8_t* kb = smem + st * C::SLOT;
@@ -809,7 +845,7 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                         if (a.nj > 0) issue_pv(J + a.nj - 1, prev_st, a.nj == 1);
                         else tc_commit(q_empty);
                         tc_commit(acc_full);
-                        trace_ev(p, o, TR_MMA1);
+                        trace_ev<TR>(p, o, TR_MMA1);
                         ks += a.nj;
                         J += a.nj;
                         ++natt;
@@ -862,7 +898,7 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                             *reinterpret_cast<uint2*>(p.x + (int64_t)t * p.ah + j) = pack_bf16x4(v);
                         }
                     }
-                    publish(p, o, et);
+                    publish<TR>(p, o, et);
                 }
             } else if (op.kind == OP_HEAD) {
                 // delta = LN_f(e).Wh + bh; a = a + s*delta (model.cpp:590-598)
@@ -928,7 +964,7 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                                 __fadd_rn(p.actions[row * 2 + 1], __fmul_rn(p.update_scale, delta1));
                         }
                     }
-                    publish(p, o, et);
+                    publish<TR>(p, o, et);
                 }
             } else if (op.kind == OP_GEMM) {
                 const bool split_path = op.splits > 1;
@@ -981,63 +1017,70 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                     const int f = g.f0 + q * 32 + lane;
                     const int fl = q * 32 + lane;  // feature within the tile
                     uint8_t* stg_base = smem + C::OFF_STG;
-                    const float bf = split_path ? 0.f : op.bias[f];
-                    const float cs = (ln_in && !split_path) ? op.colsum[f] : 0.f;
                     const int cb = hh * (TNo / 2);
-                    const int64_t ldo = split_path ? op.nf : op.ldo;
+                    // unsplit drain: per-feature constants of the fragment layout (features fa + 8k)
+                    float bfk[4] = {0.f, 0.f, 0.f, 0.f}, csk[4] = {0.f, 0.f, 0.f, 0.f};
+                    if (!split_path) {
+                        const int fa = g.f0 + q * 32 + (lane >> 2);
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) {
+                            bfk[k] = op.bias[fa + 8 * k];
+                            if (ln_in) csk[k] = op.colsum[fa + 8 * k];
+                        }
+                    }
                     mbar_wait(acc_full, nmma & 1);
-                    if (et == 0) trace_ev(p, o, TR_ACC);
+                    if (et == 0) trace_ev<TR>(p, o, TR_ACC);
                     tc_fence_after();
                     {
-                        DrainArgs da;
-                        da.tacc = tbase + lane_off + cb;
-                        da.testage = resid && !split_path ? tbase + lane_off + 256 + cb : 0xffffffffu;
-                        da.ncol = min(TNo / 2, max(0, p.M - (g.t0 + cb)));
-                        da.c0 = cb;
-                        da.fl = fl;
-                        da.q = q;
-                        da.lane = lane;
-                        da.gelu = gelu;
-                        da.bf = bf;
-                        da.cs = cs;
-                        da.mu_s = ln_in ? mu_s : nullptr;
-                        da.rs_s = rs_s;
-                        da.ldo = ldo;
-                        da.erow = f32o ? reinterpret_cast<float*>(op.out) + (int64_t)(g.t0 + cb) * ldo + f : nullptr;
-                        da.stg = stg_base;
-                        da.stg_panel = TNo * 128;
-                        da.st_part = (f32o && op.stats_out) ? st_part : nullptr;
-                        da.part = nullptr;
-                        da.dbg = 0;
                         if (!split_path) {
-                            drain(da, ln_in, gelu, resid, f32o, false);
+                            DrainArgs da;
+                            da.tacc = tbase + lane_off + cb;
+                            da.tres = tbase + lane_off + 256 + cb;
+                            da.nvalid = min(TNo / 2, max(0, p.M - (g.t0 + cb)));
+                            da.ncol = min(TNo / 2, (da.nvalid + 15) & ~15);
+                            da.cb = cb;
+                            da.q = q;
+                            da.lane = lane;
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                da.bf[k] = bfk[k];
+                                da.cs[k] = csk[k];
+                            }
+                            da.mu_s = mu_s;
+                            da.rs_s = rs_s;
+                            da.eout = f32o ? reinterpret_cast<float*>(op.out) + (int64_t)g.t0 * op.ldo + g.f0 + q * 32 : nullptr;
+                            da.ldo = op.ldo;
+                            da.stg = stg_base;
+                            da.tn = TNo;
+                            da.st_part = st_part;
+                            drain(da, ln_in, gelu, resid, f32o, f32o && op.stats_out);
                         } else {
                             // partials of the tokens other splits finalise: [cb, cb+TNo/2)
                             // minus [own_lo, own_hi), clipped to M
                             const int hi = min(cb + TNo / 2, p.M - g.t0);
                             const int r0a = cb, r0b = min(hi, own_lo);
                             const int r1a = max(cb, own_hi), r1b = hi;
-                            float* part0 = p.ws + ((int64_t)g.s * p.M + g.t0) * ldo + f;
-                            if (r0b > r0a) {
-                                da.tacc = tbase + lane_off + r0a;
-                                da.ncol = r0b - r0a;
-                                da.part = part0 + (int64_t)r0a * ldo;
-                                drain_t<false, false, false, false, false, true>(da);
-                            }
-                            if (r1b > r1a) {
-                                da.tacc = tbase + lane_off + r1a;
-                                da.ncol = r1b - r1a;
-                                da.part = part0 + (int64_t)r1a * ldo;
-                                drain_t<false, false, false, false, false, true>(da);
+                            float* blk = p.ws + ((int64_t)(g.tile * op.splits + g.s) * TNo) * 128 + fl;
+#pragma unroll 1
+                            for (int seg = 0; seg < 2; ++seg) {
+                                const int ra = seg ? r1a : r0a, rb = seg ? r1b : r0b;
+#pragma unroll 1
+                                for (int c = ra; c < rb; c += 8) {
+                                    uint32_t r[8];
+                                    tmem_ld8(tbase + lane_off + c, r);
+                                    tmem_ld_wait();
+#pragma unroll
+                                    for (int j = 0; j < 8; ++j) stg(blk + (c + j) * 128, __uint_as_float(r[j]));
+                                }
                             }
                         }
                     }
-                    if (et == 0) trace_ev(p, o, TR_LOOP);
+                    if (et == 0) trace_ev<TR>(p, o, TR_LOOP);
                     if (!split_path) {
                         // staged bf16 tile (output, or the residual's bf16 copy) -> TMA store
                         fence_proxy_async();
                         epi_bar();
-                        if (et == 0) trace_ev(p, o, TR_BAR);
+                        if (et == 0) trace_ev<TR>(p, o, TR_BAR);
                         if (et == 0) {
                             const CUtensorMap* tmo = f32o ? op.tmXB : op.tmO;
                             tma_store_2d(tmo, stg_base, g.f0, g.t0);
@@ -1045,68 +1088,54 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                             bulk_commit();
                         }
                     }
-                    if (et == 0) trace_ev(p, o, TR_DRAIN);
+                    if (et == 0) trace_ev<TR>(p, o, TR_DRAIN);
                     tc_fence_before();
                     epi_bar();
                     if (et == 0) mbar_arrive(acc_empty);
                     ++nmma;
                     if (split_path) {
-                        split_meet(p, op, o, p.splitc + op.split_base + g.tile, et);
+                        split_meet<TR>(p, op, o, p.splitc + op.split_base + g.tile, et);
                         // finalise the owned tokens in the TMEM layout: own partial from
-                        // TMEM + the other splits' partials (fixed split order) + bias
-                        // (+ staged residual) -> e, bf16 copy, row statistics
+                        // TMEM + the other splits' partials + bias (+ staged residual) ->
+                        // fp32 staging; then the row pass (stats + bf16 copy) and TMA stores
+                        const int orows = own_hi - own_lo;
+                        float* e_stg = reinterpret_cast<float*>(smem + C::OFF_STG);
+                        uint8_t* x_stg = op.xb_out ? smem + C::OFF_STG + orows * 512 : nullptr;
                         FixArgs fa;
                         fa.tacc = tbase + lane_off + my_lo;
                         fa.testage = tbase + lane_off + 256 + my_lo;
-                        fa.ncol = my_n;
-                        fa.c0 = my_lo;
-                        fa.S = op.splits;
-                        fa.s_own = g.s;
-                        fa.ws = p.ws + (int64_t)(g.t0 + my_lo) * op.nf + f;
-                        fa.split_stride = (int64_t)p.M * op.nf;
-                        fa.nf = op.nf;
+                        fa.ncol = (my_n + 7) & ~7;
+#pragma unroll
+                        for (int k = 0; k < 3; ++k) {
+                            const int sk = k < g.s ? k : k + 1;  // the other splits, by index
+                            fa.oth[k] = sk < op.splits
+                                            ? p.ws + ((int64_t)(g.tile * op.splits + sk) * TNo + my_lo) * 128 + fl
+                                            : nullptr;
+                        }
                         fa.bf = op.bias[f];
-                        // outputs staged in smem, written by TMA tensor stores below
-                        const int orows = own_hi - own_lo;
-                        const bool staged = op.tmEs != nullptr;
-                        fa.erow = reinterpret_cast<float*>(op.out) + (int64_t)(g.t0 + my_lo) * op.ldo + f;
-                        fa.xrow = op.xb_out ? op.xb_out + (int64_t)(g.t0 + my_lo) * op.ldo + f : nullptr;
-                        fa.ldo = op.ldo;
-                        fa.e_stg = staged ? reinterpret_cast<float*>(smem + C::OFF_STG) : nullptr;
-                        fa.x_stg = (staged && op.xb_out) ? smem + C::OFF_STG + orows * 512 : nullptr;
-                        fa.rows = orows;
-                        fa.r0 = my_lo - own_lo;
-                        fa.st_part = op.stats_out ? st_part : nullptr;
-                        fa.q = q;
-                        fa.lane = lane;
-                        if (resid) fix_t<true>(fa);
-                        else fix_t<false>(fa);
+                        fa.e_stg = e_stg + (my_lo - own_lo) * 128 + fl;
+                        fa.tr = (TR && p.trace && et == 0)
+                                    ? p.trace + ((size_t)o * gridDim.x + blockIdx.x) * TR_NSLOT + TR_FIXC0
+                                    : nullptr;
+                        if (resid) fix_t<true, TR>(fa);
+                        else fix_t<false, TR>(fa);
+                        if (et == 0) trace_ev<TR>(p, o, TR_FIXED);
+                        epi_bar();
+                        const int n_own = min(own_hi, p.M - g.t0) - own_lo;
+                        fix_rows(e_stg, x_stg, orows, n_own,
+                                 op.stats_out ? op.stats_out + (int64_t)(g.t0 + own_lo) * p.nft + g.f0 / 128 : nullptr,
+                                 p.nft, et);
                         fence_proxy_async();
                         epi_bar();
-                        if (staged && et == 0 && g.t0 + own_lo < p.M) {
+                        if (et == 0 && n_own > 0) {
                             tma_store_2d(op.tmEs, smem + C::OFF_STG, g.f0, g.t0 + own_lo);
-                            if (op.xb_out) {
-                                tma_store_2d(op.tmXs, smem + C::OFF_STG + orows * 512, g.f0, g.t0 + own_lo);
-                                tma_store_2d(op.tmXs, smem + C::OFF_STG + orows * 512 + orows * 128, g.f0 + 64,
-                                             g.t0 + own_lo);
+                            if (x_stg) {
+                                tma_store_2d(op.tmXs, x_stg, g.f0, g.t0 + own_lo);
+                                tma_store_2d(op.tmXs, x_stg + orows * 128, g.f0 + 64, g.t0 + own_lo);
                             }
                             bulk_commit();
                         }
-                        if (op.stats_out) {
-                            epi_bar();
-                            const int n_own = min(own_hi, p.M - g.t0) - own_lo;
-                            if (et < n_own) {
-                                const int c = own_lo + et;
-                                float2 acc2 = st_part[c];
-#pragma unroll
-                                for (int qq = 1; qq < 4; ++qq) {
-                                    const float2 v2 = st_part[qq * 256 + c];
-                                    acc2.x += v2.x;
-                                    acc2.y += v2.y;
-                                }
-                                op.stats_out[(int64_t)(g.t0 + c) * p.nft + g.f0 / 128] = acc2;
-                            }
-                        }
+                        if (et == 0) trace_ev<TR>(p, o, TR_STORE);
                     } else if (f32o && op.stats_out) {
                         // (sum, sumsq) of each row over this 128-feature tile: the 4
                         // lane quarters in a fixed order (deterministic)
@@ -1121,7 +1150,7 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                             op.stats_out[(int64_t)(g.t0 + et) * p.nft + g.f0 / 128] = acc2;
                         }
                     }
-                    publish(p, o, et);
+                    publish<TR>(p, o, et);
                 }
             } else if (op.kind == OP_ATTN) {
                 const int i = q * 32 + lane;  // query row within the tile
@@ -1134,6 +1163,7 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                     for (int j = 0; j < a.nj; ++j) {
                         const uint32_t JJ = J + j, b = JJ & 1;
                         mbar_wait(&s_full[b], (JJ >> 1) & 1);
+                        if (j == 0 && et == 0) trace_ev<TR>(p, o, TR_SM0);
                         tc_fence_after();
                         uint32_t sr[32];
                         tmem_ld32(tS[b] + lane_off + hh * 32, sr);
@@ -1203,12 +1233,13 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                         mbar_arrive(&p_full[b]);
                     }
                     J += a.nj;
+                    if (et == 0) trace_ev<TR>(p, o, TR_SMX);
                     // merge the two key halves of each row inside the CTA: exchange
                     // (m, l) through smem, then thread (row, half) combines dims
                     // [half*HD/2, (half+1)*HD/2) of O_A and O_B from TMEM
                     // (scratch overlaps the P tiles: only after the last PV completed)
                     mbar_wait(acc_full, nmma & 1);
-                    if (et == 0) trace_ev(p, o, TR_ACC);
+                    if (et == 0) trace_ev<TR>(p, o, TR_ACC);
                     tc_fence_after();
                     float* mlx = reinterpret_cast<float*>(smem + C::OFF_SCR);  // [2][2][128]
                     mlx[(hh * 2 + 0) * 128 + i] = m_ref;
@@ -1223,6 +1254,11 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                     const bool final_out = op.splits == 1;
                     const float sc = final_out ? 1.0f / lsum : 1.0f;
                     constexpr int DH = HD / 2;  // dims per thread
+                    // KV-split partials: staged as fp32 SW128 panels of 32 dims ([HD/32][128 rows][128 B],
+                    // the Q/P region: every MMA of the item has completed) and written by TMA
+                    // stores -- thread-per-row global stores would scatter 32 rows per instruction
+                    uint8_t* pst = smem + C::OFF_Q;
+                    if (!final_out) epi_bar();  // the (m, l) scratch is read before the staging overwrites it
 #pragma unroll 1
                     for (int cc = 0; cc < DH; cc += 16) {
                         uint32_t oa[16], ob[16];
@@ -1233,32 +1269,49 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
 #pragma unroll
                         for (int e2 = 0; e2 < 16; ++e2)
                             v[e2] = (w0 * __uint_as_float(oa[e2]) + w1 * __uint_as_float(ob[e2])) * sc;
-                        if (t < p.M) {
-                            if (final_out) {
+                        if (final_out) {
+                            if (t < p.M) {
                                 __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(op.out) + (int64_t)t * p.kv + a.h * HD + hh * DH + cc;
 #pragma unroll
                                 for (int e2 = 0; e2 < 16; e2 += 4)
                                     *reinterpret_cast<uint2*>(dst + e2) = pack_bf16x4(make_float4(v[e2], v[e2 + 1], v[e2 + 2], v[e2 + 3]));
-                            } else {
-                                float* dst = p.ws + ((int64_t)a.s * p.M + t) * p.kv + a.h * HD + hh * DH + cc;
+                            }
+                        } else {
+                            const int d0 = hh * DH + cc;  // 16 dims = 4 chunks of one 32-dim panel
+                            uint8_t* prow = pst + (d0 >> 5) * (128 * 128) + i * 128;
 #pragma unroll
-                                for (int e2 = 0; e2 < 16; e2 += 4)
-                                    *reinterpret_cast<float4*>(dst + e2) = make_float4(v[e2], v[e2 + 1], v[e2 + 2], v[e2 + 3]);
+                            for (int e2 = 0; e2 < 16; e2 += 4) {
+                                const int ch = ((d0 & 31) + e2) >> 2;
+                                *reinterpret_cast<float4*>(prow + ((ch ^ (i & 7)) << 4)) =
+                                    make_float4(v[e2], v[e2 + 1], v[e2 + 2], v[e2 + 3]);
                             }
                         }
                     }
                     if (hh == 0 && t < p.M && !final_out) p.wsml[((int64_t)a.s * p.M + t) * p.H + a.h] = make_float2(mm, lsum);
+                    if (!final_out) {
+                        fence_proxy_async();
+                        epi_bar();
+                        if (et == 0) {
+#pragma unroll 1
+                            for (int pn = 0; pn < HD / 32; ++pn)
+                                tma_store_3d(op.tmXs, pst + pn * (128 * 128), a.h * HD + pn * 32, a.row0, a.s);
+                            bulk_commit();
+                            bulk_wait_all();
+                            fence_proxy_async_global();
+                        }
+                    }
+                    if (et == 0) trace_ev<TR>(p, o, TR_MERGE);
                     tc_fence_before();
                     epi_bar();
                     if (et == 0) mbar_arrive(acc_empty);
                     ++nmma;
                     if (!final_out) {
-                        split_meet(p, op, o, p.splitc + op.split_base + a.tile, et);
+                        split_meet<TR>(p, op, o, p.splitc + op.split_base + a.tile, et);
                         const int rb = a.row0 + (a.s * 128) / op.splits;
                         const int re = min(p.M, a.row0 + ((a.s + 1) * 128) / op.splits);
-                        attn_fixup<HD>(p, op, a, rb, re, ew, lane);
+                        attn_fixup<HD>(p, op, a, rb, re, et);
                     }
-                    publish(p, o, et);
+                    publish<TR>(p, o, et);
                 }
             }
         }

@@ -51,4 +51,22 @@ void make_tmap_f32_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t
         fail(ALPA_ERR_INTERNAL, "cuTensorMapEncodeTiled (f32) failed (" + std::to_string((int)r) + ")");
 }
 
+// 3-D fp32 tensor [d2][d1][d0] (strides in bytes), box {32, box1, 1}, SWIZZLE_128B:
+// the attention KV-split partials [split][token][kv], one 128-byte swizzled
+// panel of 32 fp32 per box row; the split dimension keeps out-of-range token
+// rows of one split from landing in the next split's rows (TMA clips per dim).
+void make_tmap_f32_3d_sw128(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
+                            uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box1) {
+    cuuint64_t dims[3] = {d0, d1, d2};
+    cuuint64_t strides[2] = {stride1_bytes, stride2_bytes};
+    cuuint32_t box[3] = {32, box1, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims,
+                             strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        fail(ALPA_ERR_INTERNAL, "cuTensorMapEncodeTiled (f32 3d) failed (" + std::to_string((int)r) + ")");
+}
+
 }  // namespace alpa

@@ -26,29 +26,24 @@ __global__ void __launch_bounds__(320, 1) drain_kernel(int mode, long long* out_
         const int cb = hh * 96;
         DrainArgs da;
         da.tacc = tbase + ((uint32_t)(q * 32) << 16) + cb;
-        da.testage = (mode & 4) ? tbase + ((uint32_t)(q * 32) << 16) + 256 + cb : 0xffffffffu;
+        da.tres = tbase + ((uint32_t)(q * 32) << 16) + 256 + cb;
         da.ncol = 96;
-        da.c0 = cb;
-        da.fl = q * 32 + lane;
+        da.nvalid = 96;
+        da.cb = cb;
         da.q = q;
         da.lane = lane;
-        da.gelu = (mode & 1) ? 1 : 0;
-        da.bf = 0.1f;
-        da.cs = 0.2f;
-        da.mu_s = (mode & 2) ? mu_s : nullptr;
+        for (int k = 0; k < 4; ++k) { da.bf[k] = 0.1f * k; da.cs[k] = 0.5f; }
+        da.mu_s = mu_s;
         da.rs_s = rs_s;
-        da.erow = (mode & 8) ? gout + (size_t)blockIdx.x * 192 * 2048 + cb * 2048 + q * 32 + lane : nullptr;
+        da.eout = (mode & 8) ? gout + (size_t)blockIdx.x * 192 * 2048 + q * 32 : nullptr;
         da.ldo = 2048;
         da.stg = smem;
-        da.stg_panel = 192 * 128;
-        da.st_part = (mode & 8) ? st_part : nullptr;
-        da.part = nullptr;
-        da.dbg = (mode & 16) ? 1 : 0;
-        if (mode & 32) da.dbg |= 2;
+        da.tn = 192;
+        da.st_part = st_part;
         for (int rep = 0; rep < 4; ++rep) {
             asm volatile("bar.sync 1, 256;");
             const long long t0 = clock64();
-            drain(da, mode & 2, mode & 1, mode & 4, mode & 8, false);
+            drain(da, mode & 2, mode & 1, mode & 4, mode & 8, mode & 8);
             asm volatile("bar.sync 1, 256;");
             const long long t1 = clock64();
             if (threadIdx.x == 64) out_cycles[blockIdx.x * 4 + rep] = t1 - t0;
@@ -66,7 +61,7 @@ int main() {
     cudaMalloc(&g, (size_t)128 * 192 * 2048 * 4);
     cudaFuncSetAttribute(drain_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
     
-    for (int mode : {0, 16, 32, 48, 3, 19, 35, 51}) {
+    for (int mode : {0, 1, 2, 3, 12}) {
         drain_kernel<<<128, 320, 100 * 1024>>>(mode, d, g);
         cudaDeviceSynchronize();
         long long h[512];

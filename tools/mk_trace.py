@@ -20,6 +20,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--blocks", type=int, default=4)
 ap.add_argument("--n", type=int, default=6)
 ap.add_argument("--r", type=int, default=2048)
+ap.add_argument("--dump", default="", help="save the raw per-CTA trace (npz)")
+ap.add_argument("--extra", action="store_true", help="split finalisation / attention merge sub-phases")
 a = ap.parse_args()
 cfg = alpa.ModelConfig(vision_blocks=0, hidden_dim=64, vocab_size=128, decoder_blocks=a.blocks,
                        action_hidden_dim=2048, kv_dim=1024, heads=8, diffusion_iters=2, dtype="bf16")
@@ -39,11 +41,18 @@ nops, grid = C.c_int64(), C.c_int64()
 rc = L.alpa_debug_mk_trace(g._h, buf.ctypes.data_as(C.POINTER(C.c_ulonglong)), buf.size,
                            C.byref(nops), C.byref(grid))
 assert rc == 0, rc
-tr = buf[: nops.value * grid.value * 16].reshape(nops.value, grid.value, 16).astype(np.int64)
+NS = 32  # mk::TR_NSLOT
+tr = buf[: nops.value * grid.value * NS].reshape(nops.value, grid.value, NS).astype(np.int64)
+if a.dump:
+    np.savez_compressed(a.dump, trace=tr)
 names = [p["name"][5:] for p in prof if p["name"].startswith("span:")]
 spans = {p["name"][5:]: p for p in prof if p["name"].startswith("span:")}
 ev = ["dep", "mma1", "acc", "acc9", "loop", "loop9", "bar", "drain", "meet", "fix", "pub"]
 order = [0, 2, 3, 12, 10, 13, 11, 7, 4, 8, 5]
+if a.extra:
+    ev = ["dep", "mma0", "sm0", "smx", "mma1", "acc", "loop", "merge", "meet", "fixin", "fixv0", "fixc0", "fixc1", "fixc2", "fixed", "store", "stats",
+          "fix", "fence", "pub"]
+    order = [0, 1, 25, 26, 2, 3, 10, 22, 4, 23, 24, 16, 17, 18, 19, 20, 21, 8, 9, 5]
 t0 = tr[tr > 0].min()
 prev_done = t0
 tags = []
