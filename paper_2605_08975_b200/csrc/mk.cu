@@ -162,6 +162,14 @@ void mk_prepare(Ctx& c, int64_t n) {
     // split op pays an fp32 partial round trip through L2, so only the deep-K
     // MLP2 (K = 4 ah) splits by default
     int cap[6] = {1, 1, 1, 4, 1, 4};
+    // L2 prefetch (cp.async.bulk.prefetch.L2, 1/G per CTA) of the next op's bytes,
+    // per issuing op kind: bit 0 QKV -> its block's prefix K/V, 1 O -> MLP1 weights,
+    // 2 MLP1 -> MLP2, 3 MLP2 -> next QKV, 4/5 encoder MLPs, 6 attention -> O weights.
+    // The GEMM mainloops are bound by L2 -> SM throughput, not HBM: a prefetch issued
+    // during a GEMM competes with it and slows the epilogues' L2 traffic (measured,
+    // all on: +0.9 ms/scene).  Only attention (not L2-bound) pulls the O weights ahead.
+    int pf_mask = 0x40;
+    if (const char* e = getenv("ALPA_MK_PF")) pf_mask = (int)strtol(e, nullptr, 0);
     if (const char* e = getenv("ALPA_MK_SPLITS"))
         std::sscanf(e, "%d,%d,%d,%d,%d,%d", &cap[0], &cap[1], &cap[2], &cap[3], &cap[4], &cap[5]);
     auto gemm = [&](const Linear& L, int mw, void* xin, int epi, void* out, int64_t ldo, bool produce,
@@ -213,8 +221,9 @@ void mk_prepare(Ctx& c, int64_t n) {
             op.xb_out = (__nv_bfloat16*)c.ws.x;
         }
         if (consume) op.stats_in = stats;
+        // L2 prefetch of a later op's bytes, per op kind (bit = kind, ALPA_MK_PF)
         op.pf_ptr = pf;
-        op.pf_bytes = pfb;
+        op.pf_bytes = (pf_mask >> kind) & 1 ? pfb : 0;
         // split partials: [tile][split][TN rows][128 features] fp32 blocks
         if (op.splits > 1) ws_floats = std::max(ws_floats, (size_t)tiles * op.splits * ttn * 128);
         push(op, tag, 2.0 * M * L.in * L.out);
@@ -261,7 +270,7 @@ void mk_prepare(Ctx& c, int64_t n) {
             op.pre_k_row = blkrow * r;
             op.pre_v_row = (blkrow + 1) * r;
             op.pf_ptr = blk.o.w;
-            op.pf_bytes = wb(blk.o);
+            op.pf_bytes = (pf_mask >> 6) & 1 ? wb(blk.o) : 0;
             if (op.splits > 1) {
                 // partial staging reuses the Q/P smem: one item per CTA (a next item's Q
                 // load could otherwise land on it)
