@@ -118,14 +118,23 @@ void mk_prepare(Ctx& c, int64_t n) {
         act_cache.push_back({{base, inner}, {rows, id}});
         return id;
     };
-    // token tile per op kind (qkv, o, mlp1, mlp2, enc1, enc2): the few-tile ops
-    // (QKV: 24 feature tiles, O: 16) use half tiles to spread over more SMs
-    // (a mainloop is bound by the bytes each SM streams)
-    int tno[6] = {tn >= 128 ? tn / 2 : tn, tn >= 128 ? tn / 2 : tn, tn, tn, tn, tn};
+    // token tile per op kind (qkv, o, mlp1, mlp2, enc1, enc2).  The few-feature-tile
+    // ops (QKV: 3kv/128 tiles, O: ah/128) take the smallest tile (multiple of 32,
+    // >= 64) that still fits one wave -- at N = 6 QKV 24 x 6 = 144 items, O 16 x 6 =
+    // 96: their mainloops are bound by the bytes each SM streams, so spreading
+    // wins (measured: 64/64 -0.5 ms/scene vs 96/96); the MLPs keep the full tile.
+    auto few_tile = [&](int64_t nf) {
+        const int64_t tf = nf / 128;
+        int best = tn;
+        for (int v = tn; v >= 64; v -= 32)
+            if (tf * ((M + v - 1) / v) <= G) best = v;
+        return best;
+    };
+    int tno[6] = {few_tile(3 * kv), few_tile(ah), tn, tn, tn, tn};
     if (const char* e = getenv("ALPA_MK_TN"))
         std::sscanf(e, "%d,%d,%d,%d,%d,%d", &tno[0], &tno[1], &tno[2], &tno[3], &tno[4], &tno[5]);
     for (int& v : tno)
-        if (v <= 0 || v > tn || v % 16 || (v / 2) % 8) v = tn;
+        if (v <= 0 || v > tn || v % 32) v = tn;  // drain: 16-token chunks per warp half
     CUtensorMap t64{};
     make_tmap_bf16_2d(&t64, c.ws.qkv, 3 * kv, M, 3 * kv * 2, 64, 64);
     const int mq64 = add_map(t64);
@@ -257,7 +266,9 @@ void mk_prepare(Ctx& c, int64_t n) {
             op.tiles_t = qtiles;
             const int tiles = (int)H * qtiles;
             const int nbt_min = nbp + 1;
-            op.splits = tiles >= G ? 1 : std::max(1, std::min({G / tiles, nbt_min, 6}));
+            int smax = 6;  // attn_fixup merges at most 6 partials
+            if (const char* e = getenv("ALPA_MK_ATTN_S")) smax = std::max(1, std::min(6, atoi(e)));
+            op.splits = tiles >= G ? 1 : std::max(1, std::min({G / tiles, nbt_min, smax}));
             op.n_items = tiles * op.splits;
             op.split_base = split_ctr;
             split_ctr += tiles;
