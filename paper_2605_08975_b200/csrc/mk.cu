@@ -184,6 +184,8 @@ void mk_prepare(Ctx& c, int64_t n) {
     auto gemm = [&](const Linear& L, int mw, void* xin, int epi, void* out, int64_t ldo, bool produce,
                     bool consume, const void* pf, long long pfb, const char* tag, int kind) {
         Op op{};
+        const int pf_kind = kind;
+        if (kind > 5) kind = 3;  // kind 7: MLP2 with the prefix prefetch (pf_mask bit 7)
         const int ttn = tno[kind];
         op.tn = ttn;
         op.kind = mk::OP_GEMM;
@@ -232,7 +234,7 @@ void mk_prepare(Ctx& c, int64_t n) {
         if (consume) op.stats_in = stats;
         // L2 prefetch of a later op's bytes, per op kind (bit = kind, ALPA_MK_PF)
         op.pf_ptr = pf;
-        op.pf_bytes = (pf_mask >> kind) & 1 ? pfb : 0;
+        op.pf_bytes = (pf_mask >> pf_kind) & 1 ? pfb : 0;
         // split partials: [tile][split][TN rows][128 features] fp32 blocks
         if (op.splits > 1) ws_floats = std::max(ws_floats, (size_t)tiles * op.splits * ttn * 128);
         push(op, tag, 2.0 * M * L.in * L.out);
@@ -299,8 +301,11 @@ void mk_prepare(Ctx& c, int64_t n) {
         gemm(blk.mlp1, mblk[b * 4 + 2], c.ws.x, EPI_LN_GELU_BF16, c.ws.h1, 4 * ah, false, true, blk.mlp2.w,
              wb(blk.mlp2), "gemm_mlp1", 2);
         const bool last = b + 1 == B;
+        // bit 7: MLP2 pulls the NEXT block's prefix K/V instead of its QKV weights
+        const bool pf_pre = (pf_mask >> 7) & 1;
         gemm(blk.mlp2, mblk[b * 4 + 3], c.ws.h1, EPI_RESID_F32, c.ws.e, ah, true, false,
-             last ? nullptr : c.blocks[b + 1].qkv.w, last ? 0 : wb(c.blocks[b + 1].qkv), "gemm_mlp2", 3);
+             last ? nullptr : (pf_pre ? prefix_of(b + 1) : c.blocks[b + 1].qkv.w),
+             last ? 0 : (pf_pre ? pre_block : wb(c.blocks[b + 1].qkv)), "gemm_mlp2", pf_pre ? 7 : 3);
     }
     {
         Op op{};

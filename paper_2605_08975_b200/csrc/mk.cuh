@@ -121,7 +121,10 @@ enum TraceEv : int {
     TR_FIXV0 = 24,   // split finalisation: chunk 0 values computed (slot 8)
     TR_SM0 = 25,     // attention: first S block ready (softmax starts)
     TR_SMX = 26,     // attention: softmax loop done
-    TR_NSLOT = 32,
+    TR_SMJ = 27,     // attention: softmax of block j done (27..31, j < 5)
+    TR_SJ = 32,      // attention: S MMA of block j issued (32..36)
+    TR_LJ = 37,      // attention: K/V block j loads issued (37..41)
+    TR_NSLOT = 48,
 };
 
 template <int TN, int HD>
@@ -727,6 +730,7 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                         auto load_block = [&](int j) {
                             const uint32_t st = (ks + j) % C::STAGES;
                             uint8_t* kb = slot_acquire(ks + j);
+                            if (j < 5) trace_ev<TR>(p, o, TR_LJ + j);
                             uint8_t* vb = kb + C::KVB;
                             mbar_expect_tx(&full[st], 2 * C::KVB);
                             const int gb = a.g0 + j;
@@ -838,6 +842,7 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                                 tc_mma_bf16(tS[JJ & 1], da, db, idS, kk > 0 ? 1u : 0u);
                             }
                             tc_commit(&s_full[JJ & 1]);
+                            if (j < 5) trace_ev<TR>(p, o, TR_SJ + j);
                             if (j == a.nj - 1) tc_commit(q_empty);
                             if (j > 0) issue_pv(JJ - 1, prev_st, j == 1);
                             prev_st = st;
@@ -1171,18 +1176,30 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                         tc_fence_before();
                         mbar_arrive(&s_free[b]);
                         const int gb = a.g0 + j;
-                        int lo = 0, hi = 32;
-                        if (gb < op.nbp) {
-                            hi = min(32, p.r - gb * 64 - hh * 32);
-                        } else if ((i >> 6) != gb - op.nbp) {
-                            hi = 0;  // another lane's action keys
-                        }
+                        // keys of this (row, half) in the block: warp-uniform (a warp's 32 rows
+                        // belong to one lane: i >> 6 = q >> 1); all 32 except the prefix tail
+                        // block and the other lane's action block (none)
+                        int hi = 32;
+                        if (gb < op.nbp) hi = min(32, p.r - gb * 64 - hh * 32);
+                        else if ((i >> 6) != gb - op.nbp) hi = 0;
+                        const float* srf = reinterpret_cast<const float*>(sr);
+                        // block max of the raw scores (tree: no 32-deep dependency chain);
+                        // max(s) * scale == max(s * scale) for scale > 0
                         float mx = -INFINITY;
+                        if (hi == 32) {
+                            float t8[8];
 #pragma unroll
-                        for (int k = 0; k < 32; ++k) {
-                            const float sv = (k >= lo && k < hi) ? __uint_as_float(sr[k]) * sl2 : -INFINITY;
-                            sr[k] = __float_as_uint(sv);
-                            mx = fmaxf(mx, sv);
+                            for (int k = 0; k < 8; ++k)
+                                t8[k] = fmaxf(fmaxf(srf[4 * k], srf[4 * k + 1]), fmaxf(srf[4 * k + 2], srf[4 * k + 3]));
+                            mx = fmaxf(fmaxf(fmaxf(t8[0], t8[1]), fmaxf(t8[2], t8[3])),
+                                       fmaxf(fmaxf(t8[4], t8[5]), fmaxf(t8[6], t8[7]))) * sl2;
+                        } else if (hi > 0) {
+#pragma unroll
+                            for (int k = 0; k < 32; ++k) {
+                                if (k >= hi) sr[k] = __float_as_uint(-INFINITY);
+                                mx = fmaxf(mx, __uint_as_float(sr[k]));
+                            }
+                            mx *= sl2;
                         }
                         // lazy rescale: the reference max only moves when the block
                         // max exceeds it by > 8 (log2 units); P <= 2^8 stays exact
@@ -1193,16 +1210,22 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                             corr = ex2(m_ref - mx);
                             m_ref = mx;
                         }
-                        const float base = m_ref == -INFINITY ? 0.f : m_ref;
+                        const float nb = m_ref == -INFINITY ? 0.f : -m_ref;
                         float rsum = 0.f;
                         uint32_t pk[16];
+                        if (hi > 0) {
+                            float r4[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-                        for (int k = 0; k < 16; ++k) {
-                            const float p0 = ex2(__uint_as_float(sr[2 * k]) - base);
-                            const float p1 = ex2(__uint_as_float(sr[2 * k + 1]) - base);
-                            rsum += p0 + p1;
-                            __nv_bfloat162 b2 = __floats2bfloat162_rn(p0, p1);
-                            pk[k] = *reinterpret_cast<uint32_t*>(&b2);
+                            for (int k = 0; k < 16; ++k) {
+                                const float p0 = ex2(fmaf(srf[2 * k], sl2, nb));
+                                const float p1 = ex2(fmaf(srf[2 * k + 1], sl2, nb));
+                                r4[k & 3] += p0 + p1;
+                                pk[k] = pack_bf16x2(p0, p1);
+                            }
+                            rsum = (r4[0] + r4[1]) + (r4[2] + r4[3]);
+                        } else {
+#pragma unroll
+                            for (int k = 0; k < 16; ++k) pk[k] = 0u;
                         }
                         l = l * corr + rsum;
                         if (JJ >= 2) mbar_wait(&p_free[b], ((JJ - 2) >> 1) & 1);
@@ -1231,6 +1254,7 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                         }
                         tc_fence_before();
                         mbar_arrive(&p_full[b]);
+                        if (et == 0 && j < 5) trace_ev<TR>(p, o, TR_SMJ + j);
                     }
                     J += a.nj;
                     if (et == 0) trace_ev<TR>(p, o, TR_SMX);
