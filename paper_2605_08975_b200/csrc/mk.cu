@@ -215,6 +215,14 @@ void mk_prepare(Ctx& c, int64_t n) {
         op.tmX = dm(act_map(xin, L.in, ttn));
         op.tmO = (out == c.ws.h1 || out == c.ws.qkv) ? dm(act_map(out, L.out, ttn)) : nullptr;
         op.tmXB = produce ? dm(act_map(c.ws.x, ah, ttn)) : nullptr;
+        if (op.splits == 1 && (epi == EPI_RESID_F32 || epi == EPI_F32) && (size_t)ttn * (256 + 512) <= (size_t)tn * 256) {
+            // unsplit fp32 producer whose fp32 tile fits the staging next to the bf16 tile:
+            // TMA-stored through four SW128 panels of 32 fp32 (box {32, TN, 1})
+            CUtensorMap te{};
+            make_tmap_f32_3d_sw128(&te, out, (uint64_t)L.out, (uint64_t)M, 1, (uint64_t)ldo * 4,
+                                   (uint64_t)ldo * 4 * M, (uint32_t)ttn);
+            op.tmEs = dm(add_map(te));
+        }
         if (op.splits > 1) {
             // split finalisation: TN/S owned rows, fp32 e + bf16 copy via TMA stores
             const int orows = ttn / op.splits;

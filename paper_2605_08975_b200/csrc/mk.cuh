@@ -59,7 +59,7 @@ struct Op {
     const CUtensorMap* tmQ;  // attention: qkv box {64,128}
     const CUtensorMap* tmO;  // GEMM, unsplit bf16 output: TMA store map, box {64,TN}
     const CUtensorMap* tmXB; // GEMM, unsplit residual producer: bf16 copy map, box {64,TN}
-    const CUtensorMap* tmEs; // GEMM, split residual producer: fp32 rows, box {128, TN/S}
+    const CUtensorMap* tmEs; // GEMM fp32 producer: split -> fp32 rows, box {128, TN/S}; unsplit -> SW128 box {32, TN, 1}
     const CUtensorMap* tmXs; // GEMM, split residual producer: bf16 copy, box {64, TN/S}
                              // attention: fp32 KV-split partials [S][M][kv], box {32, 128, 1} SW128
     const float* bias;
@@ -383,6 +383,7 @@ struct DrainArgs {
     float* eout;             // fp32 output at (tile token 0, feature fa) (row stride ldo) or null
     long long ldo;
     uint8_t* stg;            // bf16 staging (two SW128 panels of [TN][128 B]) or null
+    uint8_t* estg;           // fp32 staging (four SW128 panels of [TN][32 fp32]) instead of eout, or null
     int tn;
     float2* st_part;         // row-stat partials [4][256] or null
 };
@@ -436,6 +437,20 @@ __device__ __forceinline__ void drain_t(const DrainArgs& a) {
                 v[k][m] = x;
             }
         if constexpr (F32) {
+            if (a.estg) {
+                // fp32 tile -> SW128 staging (TMA-stored): the 8 rows x 2 chunks a warp
+                // writes per register land on distinct banks; no scattered global stores
+#pragma unroll
+                for (int m = 0; m < 4; ++m) {
+                    const int r = a.cb + c + (m >> 1) * 8 + 2 * tq + (m & 1);
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        const int fq = a.q * 32 + tr + 8 * k;  // feature within the tile
+                        *reinterpret_cast<float*>(a.estg + (fq >> 5) * (a.tn * 128) + r * 128 +
+                                                  (((((fq & 31) >> 2) ^ (r & 7))) << 4) + (fq & 3) * 4) = v[k][m];
+                    }
+                }
+            } else {
 #pragma unroll
             for (int m = 0; m < 4; ++m) {
                 const int tl = c + (m >> 1) * 8 + 2 * tq + (m & 1);  // token within the half
@@ -444,6 +459,7 @@ __device__ __forceinline__ void drain_t(const DrainArgs& a) {
 #pragma unroll
                     for (int k = 0; k < 4; ++k) stg(d + 8 * k, v[k][m]);
                 }
+            }
             }
         }
         if (a.stg) {
@@ -1056,6 +1072,8 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                             da.eout = f32o ? reinterpret_cast<float*>(op.out) + (int64_t)g.t0 * op.ldo + g.f0 + q * 32 : nullptr;
                             da.ldo = op.ldo;
                             da.stg = stg_base;
+                            // unsplit residual producer with a staged fp32 map: e rows after the bf16 tile
+                            da.estg = (f32o && op.tmEs) ? stg_base + TNo * 256 : nullptr;
                             da.tn = TNo;
                             da.st_part = st_part;
                             drain(da, ln_in, gelu, resid, f32o, f32o && op.stats_out);
@@ -1090,6 +1108,11 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                             const CUtensorMap* tmo = f32o ? op.tmXB : op.tmO;
                             tma_store_2d(tmo, stg_base, g.f0, g.t0);
                             tma_store_2d(tmo, stg_base + TNo * 128, g.f0 + 64, g.t0);
+                            if (f32o && op.tmEs) {
+#pragma unroll 1
+                                for (int pn = 0; pn < 4; ++pn)
+                                    tma_store_3d(op.tmEs, stg_base + TNo * 256 + pn * (TNo * 128), g.f0 + 32 * pn, g.t0, 0);
+                            }
                             bulk_commit();
                         }
                     }
