@@ -13,7 +13,7 @@ ALPA_MK=0 timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > 
 # per-op spans inside the persistent kernel (globaltimer trace)
 ALPA_MK_TRACE=1 timeout 120 python tools/mk_trace.py --blocks 4 > $out/mk_trace.txt 2>&1
 # launch list of one bench run (all launches of the timed scenes)
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --launch-skip 200 -c 120 --csv \
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:'iter_kernel|rollout' -c 40 --csv \
     --log-file $out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline > $out/ncu_launch.log 2>&1
 # full capture of one persistent iteration kernel at the bench shape (36 blocks)
 timeout 1200 ncu --set full --clock-control none --import-source on -k regex:iter_kernel -s 0 -c 1 \
