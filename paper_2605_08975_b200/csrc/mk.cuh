@@ -42,7 +42,7 @@ namespace alpa {
 namespace mk {
 
 enum OpKind : int { OP_ENCODE = 0, OP_GEMM = 1, OP_ATTN = 2, OP_HEAD = 3 };
-enum MkFlags : int { MK_NO_L2PF = 1, MK_NO_PRELOAD = 2, MK_L2_NORMAL = 8 };
+enum MkFlags : int { MK_NO_L2PF = 1, MK_NO_PRELOAD = 2, MK_L2_NORMAL = 8, MK_PRE_NORMAL = 16 };
 
 struct Op {
     int kind, epi;
@@ -124,6 +124,7 @@ enum TraceEv : int {
     TR_SMJ = 27,     // attention: softmax of block j done (27..31, j < 5)
     TR_SJ = 32,      // attention: S MMA of block j issued (32..36)
     TR_LJ = 37,      // attention: K/V block j loads issued (37..41)
+    TR_FJ = 42,      // attention: K/V block j landed at the MMA issuer (42..46)
     TR_NSLOT = 48,
 };
 
@@ -688,6 +689,7 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
             // weights and the prefix are streamed once per iteration: evict_first
             // keeps them from displacing the kernel's code and the activations in L2
             const uint64_t wpol = (p.flags & MK_L2_NORMAL) ? policy_evict_normal() : policy_evict_first();
+            const uint64_t ppol = (p.flags & MK_PRE_NORMAL) ? policy_evict_normal() : wpol;  // prefix K/V
             auto slot_acquire = [&](uint32_t kk) -> uint8_t* {
                 const uint32_t st = kk % C::STAGES, ph = (kk / C::STAGES) & 1;
                 mbar_wait(&empty[st], ph ^ 1);
@@ -756,9 +758,9 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                                 const int col = a.h * HD + pn * 64;
                                 if (gb < op.nbp) {
                                     tma_load_2d_hint(kb + pn * C::KPANEL, op.tmW, &full[st], col,
-                                                     (int)(op.pre_k_row + gb * 64), wpol);
+                                                     (int)(op.pre_k_row + gb * 64), ppol);
                                     tma_load_2d_hint(vb + pn * C::KPANEL, op.tmW, &full[st], col,
-                                                     (int)(op.pre_v_row + gb * 64), wpol);
+                                                     (int)(op.pre_v_row + gb * 64), ppol);
                                 } else {
                                     const int row = a.row0 + (gb - op.nbp) * 64;
                                     tma_load_2d(kb + pn * C::KPANEL, op.tmX, &full[st], p.kv + col, row);
@@ -850,6 +852,7 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                             const uint32_t st = (ks + j) % C::STAGES, ph = ((ks + j) / C::STAGES) & 1;
                             mbar_wait(&full[st], ph);
                             if (j == 0) trace_ev<TR>(p, o, TR_MMA0);
+                            if (j < 5) trace_ev<TR>(p, o, TR_FJ + j);
                             if (JJ >= 2) mbar_wait(&s_free[JJ & 1], ((JJ - 2) >> 1) & 1);
                             tc_fence_after();
                             const uint8_t* kb = smem + st * C::SLOT;

@@ -8,7 +8,7 @@ prev = tr[base][:, 5].max()  # qkv done
 row = tr[base + 1]
 act = row[:, 5] > 0
 cols = [('dep', 0), ('mma0', 1), ('sm0', 25)] + [(f'L{j}', 37 + j) for j in range(5)] + \
-       [(f'S{j}', 32 + j) for j in range(5)] + [(f'P{j}', 27 + j) for j in range(5)] + \
+       [(f'F{j}', 42 + j) for j in range(5)] + [(f'S{j}', 32 + j) for j in range(5)] + [(f'P{j}', 27 + j) for j in range(5)] + \
        [('smx', 26), ('acc', 3), ('merge', 22), ('meet', 4), ('fix', 8), ('pub', 5)]
 for nm, i in cols:
     v = row[act, i]
