@@ -351,12 +351,6 @@ __device__ inline dd dd_mul_d(dd a, double b) {
     e = __dadd_rn(e, __dmul_rn(a.lo, b));
     return quick_two_sum(p, e);
 }
-__device__ inline dd dd_div_d(dd a, double b) {
-    const double q1 = __ddiv_rn(a.hi, b);
-    const dd p = {__dmul_rn(q1, b), __fma_rn(q1, b, -__dmul_rn(q1, b))};
-    const double r = __dadd_rn(__dsub_rn(__dsub_rn(a.hi, p.hi), p.lo), a.lo);
-    return quick_two_sum(q1, __ddiv_rn(r, b));
-}
 
 __device__ void sincos_dd(double x, double* sn, double* cs) {
     // Cody-Waite reduction by pi/2 with a 3-part constant (fdlibm split).
@@ -368,17 +362,39 @@ __device__ void sincos_dd(double x, double* sn, double* cs) {
     r = dd_add(r, dd{-__dmul_rn(k, p3), -__fma_rn(k, p3, -__dmul_rn(k, p3))});
     r = dd_add(r, dd{-__dmul_rn(k, p3t), 0.0});
     const dd r2 = dd_mul(r, r);
-    // Taylor series to degree 27 / 26 (|r| <= pi/4: truncation < 1e-31 rel).
-    dd term = r, s = r;
-    for (int n = 3; n <= 27; n += 2) {
-        term = dd_div_d(dd_mul(term, r2), -(double)((n - 1) * n));
-        s = dd_add(s, term);
-    }
-    dd tc = {1.0, 0.0}, c = {1.0, 0.0};
-    for (int n = 2; n <= 26; n += 2) {
-        tc = dd_div_d(dd_mul(tc, r2), -(double)((n - 1) * n));
-        c = dd_add(c, tc);
-    }
+    const double z = r2.hi;
+    // Taylor series to degree 27 / 26 (|r| <= pi/4: truncation < 1e-31 rel).  The
+    // terms from r^13 / r^12 on are < 1e-10 of the result: summed in double (Horner
+    // in r^2, error < 1e-26 relative); the head in double-double with exact
+    // double-double coefficients (-1)^k / n! -- no divisions, one rounding at the end.
+    double ts = -9.183689863795546e-29;
+    ts = __fma_rn(ts, z, 6.446950284384474e-26);
+    ts = __fma_rn(ts, z, -3.868170170630684e-23);
+    ts = __fma_rn(ts, z, 1.9572941063391263e-20);
+    ts = __fma_rn(ts, z, -8.22063524662433e-18);
+    ts = __fma_rn(ts, z, 2.8114572543455206e-15);
+    ts = __fma_rn(ts, z, -7.647163731819816e-13);
+    ts = __fma_rn(ts, z, 1.6059043836821613e-10);
+    double tc = -2.4795962632247976e-27;
+    tc = __fma_rn(tc, z, 1.6117375710961184e-24);
+    tc = __fma_rn(tc, z, -8.896791392450574e-22);
+    tc = __fma_rn(tc, z, 4.110317623312165e-19);
+    tc = __fma_rn(tc, z, -1.5619206968586225e-16);
+    tc = __fma_rn(tc, z, 4.779477332387385e-14);
+    tc = __fma_rn(tc, z, -1.1470745597729725e-11);
+    tc = __fma_rn(tc, z, 2.08767569878681e-09);
+    dd qs = dd_add(dd{-2.505210838544172e-08, 1.448814070935912e-24}, dd_mul_d(r2, ts));
+    dd qc = dd_add(dd{-2.755731922398589e-07, -2.3767714622250297e-23}, dd_mul_d(r2, tc));
+    qs = dd_add(dd{2.7557319223985893e-06, -1.858393274046472e-22}, dd_mul(r2, qs));
+    qc = dd_add(dd{2.48015873015873e-05, 2.1511947866775882e-23}, dd_mul(r2, qc));
+    qs = dd_add(dd{-0.0001984126984126984, -1.7209558293420705e-22}, dd_mul(r2, qs));
+    qc = dd_add(dd{-0.001388888888888889, 5.300543954373577e-20}, dd_mul(r2, qc));
+    qs = dd_add(dd{0.008333333333333333, 1.1564823173178714e-19}, dd_mul(r2, qs));
+    qc = dd_add(dd{0.041666666666666664, 2.3129646346357427e-18}, dd_mul(r2, qc));
+    qs = dd_add(dd{-0.16666666666666666, -9.25185853854297e-18}, dd_mul(r2, qs));
+    qc = dd_add(dd{-0.5, 0.0}, dd_mul(r2, qc));
+    const dd s = dd_add(r, dd_mul(r, dd_mul(r2, qs)));   // r + r^3 (s3 + r^2 (...))
+    const dd c = dd_add(dd{1.0, 0.0}, dd_mul(r2, qc));   // 1 + r^2 (c2 + r^2 (...))
     const double sh = __dadd_rn(s.hi, s.lo), ch = __dadd_rn(c.hi, c.lo);
     const long q = ((long)k) & 3;
     if (q == 0) { *sn = sh; *cs = ch; }
