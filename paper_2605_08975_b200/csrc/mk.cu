@@ -255,7 +255,8 @@ void mk_prepare(Ctx& c, int64_t n) {
     {
         Op op{};
         op.kind = mk::OP_ENCODE;
-        op.n_items = (int)((M + 7) / 8);
+        op.tn = (int)std::max<int64_t>(1, (M + G - 1) / G);  // rows per item: spread over every SM
+        op.n_items = (int)((M + op.tn - 1) / op.tn);
         push(op, "encode", 4.0 * M * ah);
     }
     gemm(c.mlp1, menc1, c.ws.x, EPI_GELU_BF16, c.ws.h1, 4 * ah, false, false, c.mlp2.w, wb(c.mlp2),

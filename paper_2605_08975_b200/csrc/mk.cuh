@@ -895,7 +895,7 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                 // e0 = a.W_in + b_in + pos (model.cpp:558-559), reference rounding order;
                 // thread = 4 consecutive features, all loads of a pass in flight
                 for (int it = blockIdx.x; it < op.n_items; it += gridDim.x) {
-                    const int r0 = it * 8, r1 = min(p.M, r0 + 8);
+                    const int r0 = it * op.tn, r1 = min(p.M, r0 + op.tn);  // op.tn = rows per item
                     const int groups = (r1 - r0) * (p.ah / 4);
                     for (int gi0 = et; gi0 < groups; gi0 += 4 * 256) {
                         float4 w0[4], w1[4], bb[4], ps[4];
