@@ -283,7 +283,7 @@ def test_bf16_attention_kv_splits(port, monkeypatch, r, splits):
 
 
 # ----------------------------------------------------------------- persistent kernel
-@pytest.mark.parametrize("n,B,K,r", [(6, 2, 2, 300), (3, 1, 1, 700)])
+@pytest.mark.parametrize("n,B,K,r", [(6, 2, 2, 300), (3, 1, 1, 700), (5, 1, 2, 200), (11, 1, 1, 130)])
 def test_persistent_kernel_vs_per_op_path(port, monkeypatch, n, B, K, r):
     """The persistent iteration kernel (default) and the per-op kernel sequence
     (ALPA_MK=0) compute the same iteration: both within the bf16 bar of the
