@@ -28,9 +28,10 @@
 // on a per-tile counter and each reduces 1/S of the tile's rows in a FIXED
 // split order, so results are deterministic (graph == eager bitwise).
 //
-// Warp roles (320 threads): warp 0 TMA producer, warp 1 TMEM allocator + MMA
-// issuer, warps 2..9 epilogue / softmax / elementwise (256 threads; TMEM lane
-// quarter = warp & 3, column half = (warp - 2) >> 2).
+// Warp roles (384 threads, 3 warpgroups): warp 0 TMA producer, warp 1 TMEM
+// allocator + MMA issuer, warps 2-3 idle (warpgroup 0 gives its registers to
+// the epilogue via setmaxnreg), warps 4..11 epilogue / softmax / elementwise
+// (256 threads; TMEM lane quarter = warp & 3, column half = (warp - 4) >> 2).
 #pragma once
 
 #include "common.cuh"
@@ -157,7 +158,12 @@ struct Cfg {
     static constexpr int OFF_SCR = OFF_Q + STG_BYTES;
     static constexpr int OFF_BAR = OFF_Q + AUX;
     static constexpr int SMEM = OFF_BAR + BAR_BYTES + 1024;
-    static constexpr int THREADS = 320;
+    static constexpr int THREADS = 384;
+    // setmaxnreg split of the launch allocation (384 x 168): warpgroup 0 (the
+    // single-thread TMA / MMA roles) drops to 104, the 8 epilogue warps rise to
+    // 200 (128 * 64 freed >= 256 * 32 taken; an inc the pool cannot cover blocks)
+    static constexpr int REG_LO = 104;
+    static constexpr int REG_HI = 200;
     static_assert(STAGES >= 2, "smem ring too small");
     static_assert(SMEM <= LIMIT, "smem budget");
 };
@@ -633,7 +639,7 @@ __device__ inline void split_meet(const Params& p, const Op& op, int o, int* ctr
 
 // ------------------------------------------------------------------ the kernel
 template <int TN, int HD, bool TR>
-__global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Params p) {
+__global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Params p) {
     using C = Cfg<TN, HD>;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -681,7 +687,11 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
     __syncthreads();
     tc_fence_after();
     const uint32_t tbase = *tmem_slot;
-
+    // register reallocation at warpgroup granularity: the epilogue's fused
+    // handlers keep every load of a pass in flight only above the 168-register
+    // launch cap (a 384-thread CTA)
+    if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(C::REG_LO));
     if (warp == 0) {
         // ================================================= TMA producer
         if (lane == 0) {
@@ -881,10 +891,17 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
             }
         }
         __syncwarp();
+    }
+    // back to the launch count for the common exit path, only after the epilogue
+    // warps have given theirs back (an early inc by the idle warps 2-3 would take
+    // the registers the epilogue's inc waits for: deadlock)
+    asm volatile("bar.sync 2, 384;" ::: "memory");
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 168;");
     } else {
+        asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(C::REG_HI));
         // ================================================= epilogue / softmax / elementwise
-        const int et = threadIdx.x - 64;   // 0..255
-        const int ew = warp - 2;           // 0..7
+        const int et = threadIdx.x - 128;  // 0..255
+        const int ew = warp - 4;           // 0..7
         const int q = warp & 3;            // TMEM lane quarter
         const int hh = ew >> 2;            // column half
         const uint32_t lane_off = uint32_t(q * 32) << 16;
@@ -1367,6 +1384,8 @@ __global__ void __launch_bounds__(320, 1) iter_kernel(const __grid_constant__ Pa
                 }
             }
         }
+        asm volatile("setmaxnreg.dec.sync.aligned.u32 168;");
+        asm volatile("bar.sync 2, 384;" ::: "memory");
     }
     tc_fence_before();
     __syncthreads();
