@@ -208,11 +208,12 @@ __device__ __forceinline__ void wait_count(const int* ctr, int want) {
     uint32_t n = 0;
     while (ld_acquire(ctr) < want) {
         if (++n > (1u << 26)) {
-            // the traced twin names the stalled counter; the production kernel keeps
-            // no call in its code (a call caps the setmaxnreg register budget)
-            if constexpr (TR)
-                printf("alpa mk watchdog: block %d thread %d waits counter %p = %d < %d\n", blockIdx.x, threadIdx.x,
-                       (const void*)ctr, ld_relaxed(ctr), want);
+            // no call in the kernel's code (a call caps the setmaxnreg register budget):
+            // the message naming the stalled counter is a debug build option
+#ifdef ALPA_MK_WATCHDOG_PRINTF
+            printf("alpa mk watchdog: block %d thread %d waits counter %p = %d < %d\n", blockIdx.x, threadIdx.x,
+                   (const void*)ctr, ld_relaxed(ctr), want);
+#endif
             __trap();
         }
     }
