@@ -544,40 +544,43 @@ __device__ __forceinline__ void fix_t(const FixArgs& a) {
     const float* o1 = a.oth[1];
     const float* o2 = a.oth[2];
     float* d = a.e_stg;
-    // software-pipelined: the next chunk's 24 partial loads are in flight while
-    // this chunk is summed (needs the epilogue warps' 200-register budget)
-    float p[3][8], nx[3][8];
-    auto load = [&](int c, float (&dst)[3][8]) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            dst[0][j] = o0 ? __ldcg(o0 + (c + j) * 128) : 0.f;
-            dst[1][j] = o1 ? __ldcg(o1 + (c + j) * 128) : 0.f;
-            dst[2][j] = o2 ? __ldcg(o2 + (c + j) * 128) : 0.f;
-        }
-    };
-    if (a.ncol > 0) load(0, p);
+    // batches of 3 chunks (24 tokens: all a thread owns at TN 192, S 4): every
+    // partial load of a batch is issued before the first is used -- one L2 round
+    // trip per batch (needs the epilogue warps' 200-register budget)
 #pragma unroll 1
-    for (int c = 0; c < a.ncol; c += 8) {
-        if (c + 8 < a.ncol) load(c + 8, nx);
-        uint32_t r[8], rv[8];
-        tmem_ld8(a.tacc + c, r);
-        if constexpr (RESID) tmem_ld8(a.testage + c, rv);
-        tmem_ld_wait();
+    for (int c0 = 0; c0 < a.ncol; c0 += 24) {
+        float pv[3][3][8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-            float acc = __uint_as_float(r[j]);
-            if (o0) acc += p[0][j];
-            if (o1) acc += p[1][j];
-            if (o2) acc += p[2][j];
-            float x = acc + a.bf;
-            if constexpr (RESID) x = __uint_as_float(rv[j]) + x;
-            d[(c + j) * 128] = x;
+        for (int ch = 0; ch < 3; ++ch) {
+            const int c = c0 + ch * 8;
+            const bool on = c < a.ncol;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                pv[ch][0][j] = (on && o0) ? __ldcg(o0 + (c + j) * 128) : 0.f;
+                pv[ch][1][j] = (on && o1) ? __ldcg(o1 + (c + j) * 128) : 0.f;
+                pv[ch][2][j] = (on && o2) ? __ldcg(o2 + (c + j) * 128) : 0.f;
+            }
         }
-        if (TR && a.tr && c < 24) tr_now(a.tr + c / 8);
 #pragma unroll
-        for (int k = 0; k < 3; ++k)
+        for (int ch = 0; ch < 3; ++ch) {
+            const int c = c0 + ch * 8;
+            if (c >= a.ncol) break;
+            uint32_t r[8], rv[8];
+            tmem_ld8(a.tacc + c, r);
+            if constexpr (RESID) tmem_ld8(a.testage + c, rv);
+            tmem_ld_wait();
 #pragma unroll
-            for (int j = 0; j < 8; ++j) p[k][j] = nx[k][j];
+            for (int j = 0; j < 8; ++j) {
+                float acc = __uint_as_float(r[j]);
+                if (o0) acc += pv[ch][0][j];
+                if (o1) acc += pv[ch][1][j];
+                if (o2) acc += pv[ch][2][j];
+                float x = acc + a.bf;
+                if constexpr (RESID) x = __uint_as_float(rv[j]) + x;
+                d[(c + j) * 128] = x;
+            }
+            if (TR && a.tr && c < 24) tr_now(a.tr + c / 8);
+        }
     }
 }
 
