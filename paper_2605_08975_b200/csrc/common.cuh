@@ -112,6 +112,12 @@ __device__ inline void mbar_wait(uint64_t* bar, uint32_t phase) {
 }
 
 // ---------------------------------------------------------------- PTX: TMA
+// L2 prefetch of one TMA box (no smem destination, no barrier).
+__device__ inline void tma_prefetch_box_2d(const CUtensorMap* m, int c0, int c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global [%0, {%1, %2}];" ::"l"(reinterpret_cast<uint64_t>(m)),
+                 "r"(c0), "r"(c1)
+                 : "memory");
+}
 __device__ inline void tma_prefetch(const CUtensorMap* m) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(m)) : "memory");
 }

@@ -43,7 +43,7 @@ namespace alpa {
 namespace mk {
 
 enum OpKind : int { OP_ENCODE = 0, OP_GEMM = 1, OP_ATTN = 2, OP_HEAD = 3 };
-enum MkFlags : int { MK_NO_L2PF = 1, MK_NO_PRELOAD = 2, MK_L2_NORMAL = 8, MK_PRE_NORMAL = 16 };
+enum MkFlags : int { MK_NO_L2PF = 1, MK_NO_PRELOAD = 2, MK_L2_NORMAL = 8, MK_PRE_NORMAL = 16, MK_ATT_L2PF = 32 };
 
 struct Op {
     int kind, epi;
@@ -796,6 +796,17 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                         };
                         int pre = 0;
                         while (pre < a.nj && pre < C::STAGES && a.g0 + pre < op.nbp) load_block(pre++);
+                        if (p.flags & MK_ATT_L2PF) {
+                            // the item's remaining prefix blocks (beyond the ring) into L2 now,
+                            // while the ring waits for the QKV dependency
+#pragma unroll 1
+                            for (int j = pre; j < a.nj && a.g0 + j < op.nbp; ++j)
+#pragma unroll 1
+                                for (int pn = 0; pn < HD / 64; ++pn) {
+                                    tma_prefetch_box_2d(op.tmW, a.h * HD + pn * 64, (int)(op.pre_k_row + (a.g0 + j) * 64));
+                                    tma_prefetch_box_2d(op.tmW, a.h * HD + pn * 64, (int)(op.pre_v_row + (a.g0 + j) * 64));
+                                }
+                        }
                         trace_ev<TR>(p, o, TR_PRE);
                         if (!waited && op.dep >= 0) {
                             wait_count<TR>(p.done + op.dep, op.dep_count);
