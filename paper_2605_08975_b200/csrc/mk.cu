@@ -215,6 +215,10 @@ void mk_prepare(Ctx& c, int64_t n) {
         op.tmX = dm(act_map(xin, L.in, ttn));
         op.tmO = (out == c.ws.h1 || out == c.ws.qkv) ? dm(act_map(out, L.out, ttn)) : nullptr;
         op.tmXB = produce ? dm(act_map(c.ws.x, ah, ttn)) : nullptr;
+        // progressive 16-row stores of the unsplit drain (ALPA_MK_PROG=0: one store per tile)
+        const bool prog = !getenv("ALPA_MK_PROG") || getenv("ALPA_MK_PROG")[0] != '0';
+        if (prog && (op.tmO || op.tmXB))
+            op.tmO16 = dm(op.tmO ? act_map(out, L.out, 16) : act_map(c.ws.x, ah, 16));
         if (op.splits == 1 && (epi == EPI_RESID_F32 || epi == EPI_F32) && (size_t)ttn * (256 + 512) <= (size_t)tn * 256) {
             // unsplit fp32 producer whose fp32 tile fits the staging next to the bf16 tile:
             // TMA-stored through four SW128 panels of 32 fp32 (box {32, TN, 1})
@@ -222,6 +226,9 @@ void mk_prepare(Ctx& c, int64_t n) {
             make_tmap_f32_3d_sw128(&te, out, (uint64_t)L.out, (uint64_t)M, 1, (uint64_t)ldo * 4,
                                    (uint64_t)ldo * 4 * M, (uint32_t)ttn);
             op.tmEs = dm(add_map(te));
+            make_tmap_f32_3d_sw128(&te, out, (uint64_t)L.out, (uint64_t)M, 1, (uint64_t)ldo * 4,
+                                   (uint64_t)ldo * 4 * M, 16);
+            op.tmE16 = dm(add_map(te));
         }
         if (op.splits > 1) {
             // split finalisation: TN/S owned rows, fp32 e + bf16 copy via TMA stores
@@ -341,6 +348,8 @@ void mk_prepare(Ctx& c, int64_t n) {
         fix(op.tmXB);
         fix(op.tmEs);
         fix(op.tmXs);
+        fix(op.tmO16);
+        fix(op.tmE16);
     }
     m.n_ops = (int)ops.size();
     m.d_ops = (Op*)c.dalloc(ops.size() * sizeof(Op));

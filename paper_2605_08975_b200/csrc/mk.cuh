@@ -62,6 +62,8 @@ struct Op {
     const CUtensorMap* tmXB; // GEMM, unsplit residual producer: bf16 copy map, box {64,TN}
     const CUtensorMap* tmEs; // GEMM fp32 producer: split -> fp32 rows, box {128, TN/S}; unsplit -> SW128 box {32, TN, 1}
     const CUtensorMap* tmXs; // GEMM, split residual producer: bf16 copy, box {64, TN/S}
+    const CUtensorMap* tmO16; // GEMM, unsplit: bf16 output (or the residual's bf16 copy), box {64, 16}
+    const CUtensorMap* tmE16; // GEMM, unsplit fp32 staging: SW128 box {32, 16, 1}
                              // attention: fp32 KV-split partials [S][M][kv], box {32, 128, 1} SW128
     const float* bias;
     const float* colsum;     // LN-folded consumers
@@ -397,6 +399,10 @@ struct DrainArgs {
     uint8_t* stg;            // bf16 staging (two SW128 panels of [TN][128 B]) or null
     uint8_t* estg;           // fp32 staging (four SW128 panels of [TN][32 fp32]) instead of eout, or null
     int tn;
+    // progressive TMA stores: each 16-token chunk leaves as soon as the half's 4 warps staged it
+    const CUtensorMap* tm16; // bf16 box {64, 16} or null (whole-tile store after the drain)
+    const CUtensorMap* te16; // fp32 box {32, 16, 1} or null
+    int f0, t0, hh;
     float2* st_part;         // row-stat partials [4][256] or null
 };
 template <bool LN, bool GELU, bool RESID, bool F32, bool STATS>
@@ -481,6 +487,23 @@ __device__ __forceinline__ void drain_t(const DrainArgs& a) {
                 stmatrix_x4_trans(sbase + tok * 128 + ((chunk ^ (tok & 7)) << 4),
                                   pack_bf16x2(v[0][2 * g], v[0][2 * g + 1]), pack_bf16x2(v[1][2 * g], v[1][2 * g + 1]),
                                   pack_bf16x2(v[2][2 * g], v[2][2 * g + 1]), pack_bf16x2(v[3][2 * g], v[3][2 * g + 1]));
+            }
+        }
+        if (a.tm16) {
+            // this chunk's 16 rows of the half are staged by its 4 warps: store them now
+            // (the store overlaps the rest of the drain instead of trailing it)
+            fence_proxy_async();
+            asm volatile("bar.sync %0, 128;" ::"r"(3 + a.hh) : "memory");
+            if (a.q == 0 && a.lane == 0) {
+                const int r = a.cb + c;
+                tma_store_2d(a.tm16, a.stg + r * 128, a.f0, a.t0 + r);
+                tma_store_2d(a.tm16, a.stg + a.tn * 128 + r * 128, a.f0 + 64, a.t0 + r);
+                if (a.te16) {
+#pragma unroll
+                    for (int pn = 0; pn < 4; ++pn)
+                        tma_store_3d(a.te16, a.estg + pn * (a.tn * 128) + r * 128, a.f0 + 32 * pn, a.t0 + r, 0);
+                }
+                bulk_commit();
             }
         }
         if constexpr (STATS) {
@@ -623,8 +646,8 @@ __device__ inline void fix_rows(const float* e_stg, uint8_t* x_stg, int rows, in
 // (async-proxy) readers, then count the item.
 template <bool TR>
 __device__ inline void publish(const Params& p, int o, int et) {
-    if (et == 0) {
-        trace_ev<TR>(p, o, TR_FIX);
+    if ((et & 127) == 0) {  // the TMA-store issuers (et 0, and et 128 for the drain's second half)
+        if (et == 0) trace_ev<TR>(p, o, TR_FIX);
         bulk_wait_all();  // this item's TMA stores have landed
     }
     fence_proxy_async_global();
@@ -1125,6 +1148,11 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                             da.estg = (f32o && op.tmEs) ? stg_base + TNo * 256 : nullptr;
                             da.tn = TNo;
                             da.st_part = st_part;
+                            da.tm16 = op.tmO16;
+                            da.te16 = (f32o && op.tmEs) ? op.tmE16 : nullptr;
+                            da.f0 = g.f0;
+                            da.t0 = g.t0;
+                            da.hh = hh;
                             drain(da, ln_in, gelu, resid, f32o, f32o && op.stats_out);
                         } else {
                             // partials of the tokens other splits finalise: [cb, cb+TNo/2)
@@ -1148,7 +1176,7 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                         }
                     }
                     if (et == 0) trace_ev<TR>(p, o, TR_LOOP);
-                    if (!split_path) {
+                    if (!split_path && !op.tmO16) {
                         // staged bf16 tile (output, or the residual's bf16 copy) -> TMA store
                         fence_proxy_async();
                         epi_bar();
