@@ -1409,20 +1409,21 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                                 *reinterpret_cast<float4*>(prow + ((ch ^ (i & 7)) << 4)) =
                                     make_float4(v[e2], v[e2 + 1], v[e2 + 2], v[e2 + 3]);
                             }
+                            if ((d0 & 31) == 16) {
+                                // the half's 4 warps completed this 32-dim panel: store it now
+                                fence_proxy_async();
+                                asm volatile("bar.sync %0, 128;" ::"r"(3 + hh) : "memory");
+                                if (q == 0 && lane == 0) {
+                                    tma_store_3d(op.tmXs, pst + (d0 >> 5) * (128 * 128), a.h * HD + (d0 & ~31), a.row0, a.s);
+                                    bulk_commit();
+                                }
+                            }
                         }
                     }
                     if (hh == 0 && t < p.M && !final_out) p.wsml[((int64_t)a.s * p.M + t) * p.H + a.h] = make_float2(mm, lsum);
-                    if (!final_out) {
-                        fence_proxy_async();
-                        epi_bar();
-                        if (et == 0) {
-#pragma unroll 1
-                            for (int pn = 0; pn < HD / 32; ++pn)
-                                tma_store_3d(op.tmXs, pst + pn * (128 * 128), a.h * HD + pn * 32, a.row0, a.s);
-                            bulk_commit();
-                            bulk_wait_all();
-                            fence_proxy_async_global();
-                        }
+                    if (!final_out && (et & 127) == 0) {  // the two panel-store issuers
+                        bulk_wait_all();
+                        fence_proxy_async_global();
                     }
                     if (et == 0) trace_ev<TR>(p, o, TR_MERGE);
                     tc_fence_before();
