@@ -1225,19 +1225,22 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                         if (resid) fix_t<true, TR>(fa);
                         else fix_t<false, TR>(fa);
                         if (et == 0) trace_ev<TR>(p, o, TR_FIXED);
+                        // the fp32 rows leave while the row pass builds the stats and bf16 copy
+                        fence_proxy_async();
                         epi_bar();
                         const int n_own = min(own_hi, p.M - g.t0) - own_lo;
+                        if (et == 0 && n_own > 0) {
+                            tma_store_2d(op.tmEs, smem + C::OFF_STG, g.f0, g.t0 + own_lo);
+                            bulk_commit();
+                        }
                         fix_rows(e_stg, x_stg, orows, n_own,
                                  op.stats_out ? op.stats_out + (int64_t)(g.t0 + own_lo) * p.nft + g.f0 / 128 : nullptr,
                                  p.nft, et);
                         fence_proxy_async();
                         epi_bar();
-                        if (et == 0 && n_own > 0) {
-                            tma_store_2d(op.tmEs, smem + C::OFF_STG, g.f0, g.t0 + own_lo);
-                            if (x_stg) {
-                                tma_store_2d(op.tmXs, x_stg, g.f0, g.t0 + own_lo);
-                                tma_store_2d(op.tmXs, x_stg + orows * 128, g.f0 + 64, g.t0 + own_lo);
-                            }
+                        if (et == 0 && n_own > 0 && x_stg) {
+                            tma_store_2d(op.tmXs, x_stg, g.f0, g.t0 + own_lo);
+                            tma_store_2d(op.tmXs, x_stg + orows * 128, g.f0 + 64, g.t0 + own_lo);
                             bulk_commit();
                         }
                         if (et == 0) trace_ev<TR>(p, o, TR_STORE);
