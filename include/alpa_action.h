@@ -157,6 +157,12 @@ int alpa_generate(alpa_ctx* ctx, const alpa_request* req, float* actions_out,
  * HBM (d_actions [N][64][2], d_traj [N][64][3]; d_traj may be NULL). */
 int alpa_generate_device(alpa_ctx* ctx, const alpa_request* req, const float* d_noise,
                          float* d_actions, float* d_traj, alpa_stats* stats);
+/* The rollout's non-finite-action flag of the last generate call (device int,
+ * non-zero = InternalError "non-finite action", pipeline.cpp:133-135).
+ * alpa_generate checks it itself; alpa_generate_device checks it when `stats`
+ * is given (the call synchronises then) and otherwise leaves it to the caller,
+ * who reads it after synchronising the context's stream. */
+int alpa_last_rollout_flag_device(alpa_ctx* ctx, const int** flag);
 
 /* ---- measurement --------------------------------------------------------- */
 /* Per-kernel device time of `iters` eagerly launched iterations (+ rollout),

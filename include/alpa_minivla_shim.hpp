@@ -15,6 +15,7 @@
 #pragma once
 
 #include <array>
+#include <atomic>
 #include <cstdio>
 #include <string>
 #include <cstdint>
@@ -127,7 +128,19 @@ struct ReasoningOutput {
     const void* kv_device = nullptr;  // same shape, context dtype, or null
     std::int64_t n_prefix = 1;
     std::int64_t reasoning_len = 0;   // r
-    std::uint64_t version = 0;        // bump when the content changes
+    // Identity of the content, advanced by the shim itself: every new object
+    // gets a fresh id; callers that edit kv_host / the device buffer IN PLACE
+    // call touch().  run_action_generation rebinds whenever (id, version, data
+    // pointers, shape) differ from the last bind.
+    std::uint64_t id = next_id();
+    std::uint64_t version = 0;
+    void touch() { ++version; }
+
+private:
+    static std::uint64_t next_id() {
+        static std::atomic<std::uint64_t> ctr{1};
+        return ctr.fetch_add(1);
+    }
 };
 
 // Model::DiffusionResult (model.hpp:155-160), counters redefined: one graph
@@ -326,15 +339,31 @@ private:
         }
         return out;
     }
+    // Rebind unless the SAME content is bound: keyed on the object's id (fresh
+    // per ReasoningOutput, so a new object at a reused address rebinds), its
+    // version (touch()), the data pointers and the shape.
     void bind(const ReasoningOutput& r) {
-        if (bound_version_ == r.version && bound_ptr_ == &r) return;
+        const BindKey k{r.id, r.version, r.kv_device, r.kv_host.data(), r.kv_host.size(), r.n_prefix,
+                        r.reasoning_len};
+        if (bound_valid_ && k == bound_) return;
         if (r.kv_device)
             check(alpa_bind_prefix_device(ctx_, r.kv_device, r.n_prefix, r.reasoning_len), ctx_);
         else
             check(alpa_bind_prefix(ctx_, r.kv_host.data(), r.n_prefix, r.reasoning_len), ctx_);
-        bound_version_ = r.version;
-        bound_ptr_ = &r;
+        bound_ = k;
+        bound_valid_ = true;
     }
+    struct BindKey {
+        std::uint64_t id, version;
+        const void* dev;
+        const float* host;
+        size_t host_n;
+        std::int64_t n_prefix, r;
+        bool operator==(const BindKey& o) const {
+            return id == o.id && version == o.version && dev == o.dev && host == o.host &&
+                   host_n == o.host_n && n_prefix == o.n_prefix && r == o.r;
+        }
+    };
     static alpa_request to_c(const InferenceRequest& q) {
         alpa_request r{};
         r.num_trajectories = q.num_trajectories;
@@ -351,8 +380,8 @@ private:
 
     ModelConfig cfg_;
     alpa_ctx* ctx_ = nullptr;
-    std::uint64_t bound_version_ = ~0ull;
-    const ReasoningOutput* bound_ptr_ = nullptr;
+    BindKey bound_{};
+    bool bound_valid_ = false;
 };
 
 }  // namespace alpa_shim

@@ -174,12 +174,16 @@ void orc_synthetic_prefix(uint64_t seed, int64_t blocks, int64_t r, int64_t kv,
  * roundings: acc=0; acc += a[k]*b[k][j] for k = 0..K-1. */
 static void matmul_rows(const float* a, int64_t rows, int64_t K, const float* b,
                         int64_t N, float* out) {
-#pragma omp parallel for schedule(static)
-    for (int64_t i0 = 0; i0 < rows; i0 += 4) {
-        const int64_t ni = rows - i0 < 4 ? rows - i0 : 4;
-        for (int64_t j0 = 0; j0 < N; j0 += 512) {
-            const int64_t nj = N - j0 < 512 ? N - j0 : 512;
-            float acc[4][512];
+    /* 16 x 256 output blocks: the weight rows are re-read rows/16 times instead
+     * of rows/4 (the config-2 fixtures run the full 36-block depth) */
+    const int64_t nib = (rows + 15) / 16, njb = (N + 255) / 256;
+#pragma omp parallel for schedule(dynamic, 1) collapse(2)
+    for (int64_t ib = 0; ib < nib; ++ib) {
+        for (int64_t jb = 0; jb < njb; ++jb) {
+            const int64_t i0 = ib * 16, j0 = jb * 256;
+            const int64_t ni = rows - i0 < 16 ? rows - i0 : 16;
+            const int64_t nj = N - j0 < 256 ? N - j0 : 256;
+            float acc[16][256];
             for (int64_t r = 0; r < ni; ++r)
                 for (int64_t j = 0; j < nj; ++j) acc[r][j] = 0.0f;
             for (int64_t k = 0; k < K; ++k) {
@@ -281,15 +285,16 @@ static void attention(const orc_cfg* c, const float* q, const float* pk, const f
                     }
                     const float inv = 1.0f / sum;
                     for (int64_t j = 0; j < T; ++j) s[j] *= inv;
+                    /* dot_col per output dim d, ascending j.  Loop nest reordered
+                     * (j outer, d inner, one accumulator per d): every element
+                     * still sees acc=0; acc += s[j]*v[j][d] for j = 0..T-1. */
                     float* o = ctx + (l * A + i) * kd + h * hd;
-                    for (int64_t d = 0; d < hd; ++d) {
-                        float acc = 0.0f;
-                        for (int64_t j = 0; j < T; ++j) {
-                            const float* vr = j < r ? vbase + j * kd + h * hd
-                                                    : av + (l * A + (j - r)) * kd + h * hd;
-                            acc += s[j] * vr[d];
-                        }
-                        o[d] = acc;
+                    for (int64_t d = 0; d < hd; ++d) o[d] = 0.0f;
+                    for (int64_t j = 0; j < T; ++j) {
+                        const float* vr = j < r ? vbase + j * kd + h * hd
+                                                : av + (l * A + (j - r)) * kd + h * hd;
+                        const float sj = s[j];
+                        for (int64_t d = 0; d < hd; ++d) o[d] += sj * vr[d];
                     }
                 }
             }

@@ -96,10 +96,15 @@ void check_request(Ctx& c, const alpa_request& r) {
             fail(ALPA_ERR_INTERNAL, "replicate_for_batch: source cache must have batch 1");
     } else {
         // Multi topology: the cache batch must equal N (pipeline.cpp:411-413)
-        // unless an explicit lane map was bound.
-        if (c.lane_map_host.empty() && c.prefix_n != r.num_trajectories && c.prefix_n != 1)
+        // unless an explicit lane map was bound (alpa_set_lane_prefix).
+        if (c.lane_map_host.empty() && c.prefix_n != r.num_trajectories)
             fail(ALPA_ERR_INTERNAL, "kv batch does not match the requested trajectory count");
     }
+}
+
+// actions_to_trajectory's speed check (pipeline.cpp:125-127): only when a
+// trajectory is actually produced (the reference throws it in postprocessing).
+void check_v0(const alpa_request& r) {
     if (!(r.v0 >= 0.0f) || !std::isfinite(r.v0))
         fail(ALPA_ERR_INTERNAL, "actions_to_trajectory: invalid initial speed");
 }
@@ -433,6 +438,7 @@ int alpa_generate(alpa_ctx* h, const alpa_request* req, float* actions_out, floa
         cudaSetDevice(c->device);
         const alpa_request& r = *req;
         check_request(*c, r);
+        if (traj_out) check_v0(r);
         const int64_t n = r.num_trajectories, A = c->steps();
         const int64_t K = r.diffusion_iters > 0 ? r.diffusion_iters : c->cfg.diffusion_iters;
         alpa::ensure_workspace(*c, n);
@@ -463,7 +469,9 @@ int alpa_generate(alpa_ctx* h, const alpa_request* req, float* actions_out, floa
         int bad = 0;
         std::memcpy(&bad, htraj + nt, sizeof(int));
         if (actions_out) std::memcpy(actions_out, hact, na * sizeof(float));
-        if (bad) fail(ALPA_ERR_INTERNAL, "actions_to_trajectory: non-finite action");
+        // non-finite actions fail the rollout (pipeline.cpp:133-135): only an error
+        // when trajectories were requested, like the reference's postprocessing
+        if (bad && traj_out) fail(ALPA_ERR_INTERNAL, "actions_to_trajectory: non-finite action");
         if (traj_out) std::memcpy(traj_out, htraj, nt * sizeof(float));
         if (st) {
             float ms = 0.f;
@@ -485,6 +493,7 @@ int alpa_generate_device(alpa_ctx* h, const alpa_request* req, const float* d_no
         cudaSetDevice(c->device);
         const alpa_request& r = *req;
         check_request(*c, r);
+        if (d_traj) check_v0(r);
         const int64_t n = r.num_trajectories, A = c->steps();
         const int64_t K = r.diffusion_iters > 0 ? r.diffusion_iters : c->cfg.diffusion_iters;
         alpa::ensure_workspace(*c, n);
@@ -503,13 +512,27 @@ int alpa_generate_device(alpa_ctx* h, const alpa_request* req, const float* d_no
                                       cudaMemcpyDeviceToDevice, c->stream));
         if (st) {
             ALPA_CUDA(cudaEventRecord(c->ev1, c->stream));
+            // the rollout's non-finite flag (pipeline.cpp:133-135) comes back with the
+            // stats (the call synchronises anyway); without stats the device flag is
+            // readable through alpa_last_rollout_flag_device
+            int bad = 0;
+            ALPA_CUDA(cudaMemcpyAsync(&bad, c->d_scalars + 1, sizeof(int), cudaMemcpyDeviceToHost, c->stream));
             ALPA_CUDA(cudaStreamSynchronize(c->stream));
             float ms = 0.f;
             cudaEventElapsedTime(&ms, c->ev0, c->ev1);
             st->device_ms = ms;
             fill_iter_ms(*c, st);
             st->kv_bytes = kv_bytes(*c, r);
+            if (bad && d_traj) fail(ALPA_ERR_INTERNAL, "actions_to_trajectory: non-finite action");
         }
+    });
+}
+
+int alpa_last_rollout_flag_device(alpa_ctx* h, const int** flag) {
+    Ctx* c = reinterpret_cast<Ctx*>(h);
+    return guarded(c, [&] {
+        if (!c || !flag) fail(ALPA_ERR_CONFIG, "null argument");
+        *flag = reinterpret_cast<const int*>(c->d_scalars + 1);
     });
 }
 

@@ -128,7 +128,8 @@ enum TraceEv : int {
     TR_SJ = 32,      // attention: S MMA of block j issued (32..36)
     TR_LJ = 37,      // attention: K/V block j loads issued (37..41)
     TR_FJ = 42,      // attention: K/V block j landed at the MMA issuer (42..46)
-    TR_NSLOT = 48,
+    TR_SX = 48,      // attention softmax of block 1 (thread 0): S ready, S read, exps, P slot free, P stored, arrived (48..53)
+    TR_NSLOT = 64,
 };
 
 template <int TN, int HD>
@@ -715,8 +716,8 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
         mbar_init(q_empty, 1);
         for (int i = 0; i < 2; ++i) {
             mbar_init(&s_full[i], 1);
-            mbar_init(&s_free[i], 256);
-            mbar_init(&p_full[i], 256);
+            mbar_init(&s_free[i], 8);  // one arrival per epilogue warp
+            mbar_init(&p_full[i], 8);
             mbar_init(&p_free[i], 1);
         }
         fence_mbar_init();
@@ -1272,12 +1273,16 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                         const uint32_t JJ = J + j, b = JJ & 1;
                         mbar_wait(&s_full[b], (JJ >> 1) & 1);
                         if (j == 0 && et == 0) trace_ev<TR>(p, o, TR_SM0);
+                        const bool trj = TR && j == 1 && et == 0;
+                        if (trj) trace_ev<TR>(p, o, TR_SX + 0);
                         tc_fence_after();
                         uint32_t sr[32];
                         tmem_ld32(tS[b] + lane_off + hh * 32, sr);
                         tmem_ld_wait();
                         tc_fence_before();
-                        mbar_arrive(&s_free[b]);
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&s_free[b]);
+                        if (trj) trace_ev<TR>(p, o, TR_SX + 1);
                         const int gb = a.g0 + j;
                         // keys of this (row, half) in the block: warp-uniform (a warp's 32 rows
                         // belong to one lane: i >> 6 = q >> 1); all 32 except the prefix tail
@@ -1331,7 +1336,9 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                             for (int k = 0; k < 16; ++k) pk[k] = 0u;
                         }
                         l = l * corr + rsum;
+                        if (trj) trace_ev<TR>(p, o, TR_SX + 2);
                         if (JJ >= 2) mbar_wait(&p_free[b], ((JJ - 2) >> 1) & 1);
+                        if (trj) trace_ev<TR>(p, o, TR_SX + 3);
                         uint8_t* prow = smem + C::OFF_P + b * C::P_BYTES + i * 128;
 #pragma unroll
                         for (int c = 0; c < 4; ++c) {
@@ -1340,6 +1347,7 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                                 make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
                         }
                         fence_proxy_async();
+                        if (trj) trace_ev<TR>(p, o, TR_SX + 4);
                         if (__any_sync(0xffffffffu, corr != 1.f)) {
                             // O holds PV of blocks < j: wait for the last of them, rescale
                             mbar_wait(&p_free[(JJ - 1) & 1], ((JJ - 1) >> 1) & 1);
@@ -1356,7 +1364,9 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                             tmem_st_wait();
                         }
                         tc_fence_before();
-                        mbar_arrive(&p_full[b]);
+                        __syncwarp();
+                        if (lane == 0) mbar_arrive(&p_full[b]);
+                        if (trj) trace_ev<TR>(p, o, TR_SX + 5);
                         if (et == 0 && j < 5) trace_ev<TR>(p, o, TR_SMJ + j);
                     }
                     J += a.nj;
