@@ -237,7 +237,7 @@ class Ref:
         L.ref_action_generation.argtypes = [C.POINTER(Cfg), _f32p, C.c_int64, C.c_int64,
                                             C.c_uint64, C.c_uint64, C.c_int, C.c_int, C.c_int,
                                             C.c_int, _f32p, C.POINTER(C.c_double),
-                                            C.POINTER(C.c_int64)]
+                                            C.POINTER(C.c_int64), C.POINTER(C.c_double)]
         L.ref_rollout.argtypes = [_f32p, C.c_int64, C.c_float, _f32p]
         L.ref_action_weights.argtypes = [C.POINTER(Cfg), C.c_int, _f32p, C.c_int64,
                                          C.POINTER(C.c_int64)]
@@ -272,10 +272,12 @@ class Ref:
         out = np.empty((n, cfg.action_steps, 2), np.float32)
         ms = C.c_double()
         kvb = C.c_int64()
+        it = C.c_double()
         self._check(self.L.ref_action_generation(C.byref(cfg), _fp(prefix), r, n, seed, stride,
                                                  int(static_kv), int(graph), int(single),
                                                  int(parallel), _fp(out), C.byref(ms),
-                                                 C.byref(kvb)))
+                                                 C.byref(kvb), C.byref(it)))
+        self.last_iter_ms = float(it.value)  # sum of DiffusionResult::iter_ms
         return out, float(ms.value), int(kvb.value)
 
     def rollout(self, actions: np.ndarray, v0: float) -> np.ndarray:

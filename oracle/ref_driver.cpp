@@ -148,7 +148,7 @@ int ref_action_generation(const RefCfg* c, const float* prefix, std::int64_t r,
                           std::int64_t n, std::uint64_t seed, std::uint64_t stride,
                           int static_kv, int graph_exec, int topology_single,
                           int parallel_kernels, float* actions_out, double* ms_out,
-                          std::int64_t* kv_bytes_out) {
+                          std::int64_t* kv_bytes_out, double* iter_ms_sum_out) {
     return guarded([&] {
         const ModelConfig cfg = to_cfg(c);
         SubstrateOptions so;
@@ -196,6 +196,13 @@ int ref_action_generation(const RefCfg* c, const float* prefix, std::int64_t r,
                               std::chrono::steady_clock::now() - t0)
                               .count();
         if (ms_out) *ms_out = ms;
+        // DiffusionResult::iter_ms (model.hpp:155-160): the K refinement
+        // iterations alone; the rest of the region is noise + replicate_for_batch
+        if (iter_ms_sum_out) {
+            double s = 0.0;
+            for (double v : diff.iter_ms) s += v;
+            *iter_ms_sum_out = s;
+        }
         if (kv_bytes_out) *kv_bytes_out = kv_bytes;
         for (std::int64_t l = 0; l < n; ++l) {
             for (std::int64_t i = 0; i < cfg.action_steps; ++i) {

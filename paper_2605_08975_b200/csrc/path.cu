@@ -618,6 +618,14 @@ void enqueue_iteration_mk(Ctx& c, int64_t n, cudaStream_t s) {
     MkState& m = c.mk;
     ProfRec rec{"iteration", pool_event(c), pool_event(c), 0.0, 0.0};
     for (double f : m.flops) rec.flops += f;
+    {
+        // algorithmic HBM bytes of one iteration: every weight once,
+        // the shared prefix once, the action K/V written and read
+        const double ah = (double)c.ah(), kv = (double)c.kv(), B = (double)c.cfg.decoder_blocks;
+        const double eb = 2.0, A = (double)c.steps(), r = (double)c.prefix_r;
+        rec.bytes = eb * (8 * ah * ah + 2 * ah + B * (4 * ah * kv + 8 * ah * ah) + 2 * ah) +
+                    B * 2 * r * kv * eb + B * 2 * (double)n * A * kv * eb * 2;
+    }
     ALPA_CUDA(cudaMemsetAsync(m.d_tstamp, 0, m.n_ops * sizeof(unsigned long long), s));
     ALPA_CUDA(cudaMemsetAsync(m.d_tstamp + m.n_ops, 0xFF, sizeof(unsigned long long), s));
     ALPA_CUDA(cudaEventRecord(rec.a, s));

@@ -76,3 +76,58 @@ def test_two_rank_scene_matches_single_process(tmp_path):
     b = np.load(tmp_path / "single.npy")
     assert a.shape == (5, 64, 2)
     np.testing.assert_array_equal(a, b)  # global lane seeds: bit-identical
+
+
+def _scenes_worker(rank, world, port, out_dir, num_scenes):
+    import torch
+    import torch.distributed as dist
+
+    from oracle.oracle import Cfg, Port
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    port_ = Port()
+    cfg = Cfg.make(vision_blocks=1, decoder_blocks=2, hidden_dim=16, action_hidden_dim=8,
+                   kv_dim=8, heads=2, vocab_size=128, weight_seed=77, diffusion_iters=2)
+    w = port_.weights(cfg)
+    r, n = 10, 3
+    computed = []
+
+    def produce(s, buf):  # only the root produces prefixes (the reasoning stage)
+        assert rank == 0
+        buf.copy_(torch.from_numpy(port_.synthetic_prefix(4242 + 1000 * s, 2, r, 8).ravel()))
+
+    def compute(s, buf):
+        computed.append(s)
+        pre = buf.numpy().reshape(2, 2, r, 8)
+        return torch.from_numpy(port_.refine(cfg, w, pre, port_.noise(2, 1, n)))
+
+    full, mine = pdist.run_scenes(num_scenes, compute, produce,
+                                  lambda: torch.zeros(2 * 2 * r * 8, dtype=torch.float32))
+    assert computed == mine == pdist.owned_scenes(num_scenes, world, rank)
+    if rank == 0:
+        np.save(os.path.join(out_dir, "scenes.npy"), full.numpy())
+        ref = np.stack([port_.refine(cfg, w, port_.synthetic_prefix(4242 + 1000 * s, 2, r, 8),
+                                     port_.noise(2, 1, n)) for s in range(num_scenes)])
+        np.save(os.path.join(out_dir, "scenes_ref.npy"), ref)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,num_scenes", [(2, 5), (3, 7)])
+def test_batched_scenes_sharded_match_single_process(tmp_path, world, num_scenes):
+    """Config 5 plumbing: scenes round-robin over ranks, the root sends each
+    prefix point-to-point to the owner, results gathered in scene order."""
+    import torch.multiprocessing as mp
+
+    mp.spawn(_scenes_worker, args=(world, _free_port(), str(tmp_path), num_scenes), nprocs=world,
+             join=True)
+    a = np.load(tmp_path / "scenes.npy")
+    b = np.load(tmp_path / "scenes_ref.npy")
+    assert a.shape == (num_scenes, 3, 64, 2)
+    np.testing.assert_array_equal(a, b)
+
+
+def test_scene_owner_round_robin():
+    assert [pdist.scene_owner(s, 4) for s in range(6)] == [0, 1, 2, 3, 0, 1]
+    assert pdist.owned_scenes(64, 8, 3) == list(range(3, 64, 8))

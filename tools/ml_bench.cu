@@ -72,7 +72,8 @@ __device__ inline void mbar_wait_cluster(uint64_t* bar, uint32_t phase) {
 struct P {
     const CUtensorMap* tw;  // W [rows][K], box {64, 128}
     const CUtensorMap* tx;  // X [384][K], box {64, TN} (mode 0) / {64, TN/2}
-    int K, tiles_f, tiles_t, TN, wrow0, reps, wl2;
+    int K, tiles_f, tiles_t, TN, wrow0, reps, wl2, tiled, pfd, nox;
+    const uint8_t* wbase;
 };
 
 template <int MODE, int STAGES, int TNMAX>
@@ -120,14 +121,26 @@ __global__ void __launch_bounds__(192, 1) kern(const __grid_constant__ P p) {
             const int f = ii % p.tiles_f, t = ii / p.tiles_f;
             // W rows: a pair (modes 1, 2) covers 256 rows, rank r its half
             const int wrow = p.wrow0 + rep * p.tiles_f * (M ? 256 : 128) + (M ? f * 256 + rank * 128 : f * 128);
+            // tiled layout: every (128-row tile, k-block) box is one contiguous 16 KB chunk
+            auto wc0 = [&](int i) { return p.tiled ? 0 : i * 64; };
+            auto wc1 = [&](int i) { return p.tiled ? ((wrow / 128) * KB + i) * 128 : wrow; };
+            // pfd > 0: tensor-box L2 prefetch; pfd < 0: 1-D bulk prefetch of the contiguous
+            // 16 KB box (tiled layout only), -pfd k-blocks ahead
+            auto pf = [&](int i) {
+                if (p.pfd > 0) tma_prefetch_box_2d(p.tw, wc0(i), wc1(i));
+                else l2_prefetch_hint(p.wbase + (size_t)wc1(i) * 128, 16384, pol);
+            };
+            const int pd = p.pfd > 0 ? p.pfd : -p.pfd;
+            for (int i = 0; i < pd && i < KB; ++i) pf(i);
             for (int i = 0; i < KB; ++i, ++ks) {
                 const uint32_t st = ks % STAGES, ph = (ks / STAGES) & 1;
+                if (pd && i + pd < KB) pf(i + pd);
                 mbar_wait_cluster(&empty[st], ph ^ 1);
                 uint8_t* sb = smem + st * SLOT;
                 if (M == 0) {
-                    mbar_expect_tx(&full[st], WB + TN * 128);
-                    tma_load_2d_hint(sb, p.tw, &full[st], i * 64, wrow, pol);
-                    tma_load_2d(sb + WB, p.tx, &full[st], i * 64, t * TN);
+                    mbar_expect_tx(&full[st], WB + (p.nox ? 0 : TN * 128));
+                    tma_load_2d_hint(sb, p.tw, &full[st], wc0(i), wc1(i), pol);
+                    if (!p.nox) tma_load_2d(sb + WB, p.tx, &full[st], i * 64, t * TN);
                 } else if (M == 1) {
                     // own W + the full X tile (half from each CTA's multicast)
                     mbar_expect_tx(&full[st], WB + TN * 128);
@@ -138,7 +151,7 @@ __global__ void __launch_bounds__(192, 1) kern(const __grid_constant__ P p) {
                     // pair: both CTAs' bytes complete on the leader's barrier
                     const uint32_t fb = dsmem_addr(smem_u32(&full[st]), 0);
                     if (rank == 0) mbar_expect_tx(&full[st], 2 * (WB + (TN / 2) * 128));
-                    tma_load_2d_cg2(sb, p.tw, fb, i * 64, wrow, pol);
+                    tma_load_2d_cg2(sb, p.tw, fb, wc0(i), wc1(i), pol);
                     tma_load_2d_cg2(sb + WB, p.tx, fb, i * 64, t * TN + rank * (TN / 2), pol);
                 }
             }
@@ -186,14 +199,17 @@ __global__ void __launch_bounds__(192, 1) kern(const __grid_constant__ P p) {
 }
 
 template <int MODE, int STAGES, int TNMAX>
-void run(const char* name, void* W, size_t wrows_total, void* X, int K, int nf, int TN, int G, int reps = 8, int wl2 = 0) {
+void run(const char* name, void* W, size_t wrows_total, void* X, int K, int nf, int TN, int G, int reps = 8, int wl2 = 0,
+         int tiled = 0, int pfd = 0, int nox = 0) {
     constexpr int M = MODE & 7;
     constexpr int SLOT = 128 * 64 * 2 + TNMAX * 128;
     const int smem = STAGES * SLOT + 1024 + 256;
     auto fn = kern<MODE, STAGES, TNMAX>;
     cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     CUtensorMap tw, tx;
-    make_tmap_bf16_2d(&tw, W, K, wrows_total, K * 2, 64, 128);
+    if (wl2) wrows_total = (size_t)nf * reps;
+    if (tiled) make_tmap_bf16_2d(&tw, W, 64, wrows_total * (K / 64), 128, 64, 128);
+    else make_tmap_bf16_2d(&tw, W, K, wrows_total, K * 2, 64, 128);
     make_tmap_bf16_2d(&tx, X, K, 384, K * 2, 64, M ? TN / 2 : TN);
     CUtensorMap* d;
     cudaMalloc(&d, 2 * sizeof(CUtensorMap));
@@ -208,7 +224,10 @@ void run(const char* name, void* W, size_t wrows_total, void* X, int K, int nf, 
     p.tiles_t = 384 / TN;
     p.reps = reps;
     p.wl2 = wl2;
-    if (wl2) wrows_total = (size_t)nf * reps;  // one W set, re-read every launch: L2-resident
+    p.tiled = tiled;
+    p.pfd = pfd;
+    p.nox = nox;
+    p.wbase = (const uint8_t*)W;
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(G);
     cfg.blockDim = dim3(192);
@@ -243,7 +262,7 @@ void run(const char* name, void* W, size_t wrows_total, void* X, int K, int nf, 
     const int items = p.tiles_f * p.tiles_t;
     // bytes landed in smem (all CTAs): W once per (item), X once per CTA per item
     const double wbytes = (double)nf * K * 2 * p.tiles_t * reps;
-    const double xbytes = (double)384 * K * 2 * (M == 1 ? p.tiles_f * 2 : p.tiles_f) * reps;
+    const double xbytes = nox ? 0.0 : (double)384 * K * 2 * (M == 1 ? p.tiles_f * 2 : p.tiles_f) * reps;
     const double flops = 2.0 * nf * 384 * K * reps;
     printf("%-34s G=%3d items=%4d  %7.2f us/rep  ingress %5.2f TB/s (W %5.1f MB X %5.1f MB)  %6.1f TFLOP/s  %s\n", name, G,
            items, us / reps, (wbytes + xbytes) / us * 1e-6, wbytes * 1e-6, xbytes * 1e-6, flops / us * 1e-6,
@@ -298,6 +317,37 @@ int main(int argc, char** argv) {
         snprintf(nm, sizeof nm, "o 1cta TN64 S8%s", sfx); run<0, 8, 64>(nm, W, wrows, X, 1024, 2048, 64, 96, 2, wl2);
         snprintf(nm, sizeof nm, "mlp1 cg2 TN96 S8%s", sfx); run<2, 8, 96>(nm, W, wrows, X, 2048, 8192, 96, 148, 2, wl2);
         snprintf(nm, sizeof nm, "mlp1 1cta TN96 S8%s", sfx); run<0, 8, 96>(nm, W, wrows, X, 2048, 8192, 96, 148, 2, wl2);
+    }
+    } else if (which == 3) {
+    // weights from HBM: row-major vs tiled (contiguous 16 KB boxes), L2 lookahead prefetch distance
+    for (int tiled : {0, 1})
+        for (int pfd : {0, 4, 8, 16}) {
+            char nm[64];
+            snprintf(nm, sizeof nm, "mlp1 1cta TN192 S4 t%d pf%d", tiled, pfd); run<0, 4, 192>(nm, W, wrows, X, 2048, 8192, 192, 128, 2, 0, tiled, pfd);
+            snprintf(nm, sizeof nm, "mlp1 cg2 TN192 S5 t%d pf%d", tiled, pfd); run<2, 5, 192>(nm, W, wrows, X, 2048, 8192, 192, 128, 2, 0, tiled, pfd);
+            snprintf(nm, sizeof nm, "qkv 1cta TN128 S5 t%d pf%d", tiled, pfd); run<0, 5, 128>(nm, W, wrows, X, 2048, 3072, 128, 144, 2, 0, tiled, pfd);
+            snprintf(nm, sizeof nm, "qkv 1cta TN64 S8 t%d pf%d", tiled, pfd); run<0, 8, 64>(nm, W, wrows, X, 2048, 3072, 64, 144, 2, 0, tiled, pfd);
+            snprintf(nm, sizeof nm, "o 1cta TN128 S5 t%d pf%d", tiled, pfd); run<0, 5, 128>(nm, W, wrows, X, 1024, 2048, 128, 148, 2, 0, tiled, pfd);
+            snprintf(nm, sizeof nm, "o 1cta TN64 S8 t%d pf%d", tiled, pfd); run<0, 8, 64>(nm, W, wrows, X, 1024, 2048, 64, 148, 2, 0, tiled, pfd);
+        }
+    } else if (which == 4) {
+    // pure HBM weight streaming (no X, no MMA): unique rows per CTA (tiles_t = 1 via TN = 384 is not
+    // supported, so TN = 192 with 2 token tiles re-reads each W tile twice -> report both)
+    for (int G : {64, 128, 148}) {
+        char nm[64];
+        snprintf(nm, sizeof nm, "W only S4 G%d", G); run<8, 4, 192>(nm, W, wrows, X, 2048, 8192, 192, G, 2, 0, 0, 0, 1);
+        snprintf(nm, sizeof nm, "W only S8 G%d", G); run<8, 8, 64>(nm, W, wrows, X, 2048, 8192, 192, G, 2, 0, 0, 0, 1);
+        snprintf(nm, sizeof nm, "W only tiled S8 G%d", G); run<8, 8, 64>(nm, W, wrows, X, 2048, 8192, 192, G, 2, 0, 1, 0, 1);
+    }
+    } else if (which == 5) {
+    // pure HBM streaming (W only, tiled) with L2 lookahead prefetch; then the MLP1 mainloop with it
+    for (int pfd : {0, -4, -8, -16, 8}) {
+        char nm[64];
+        snprintf(nm, sizeof nm, "W only tiled S4 G128 pf%d", pfd); run<8, 4, 192>(nm, W, wrows, X, 2048, 8192, 192, 128, 2, 0, 1, pfd, 1);
+        snprintf(nm, sizeof nm, "W only tiled S8 G128 pf%d", pfd); run<8, 8, 64>(nm, W, wrows, X, 2048, 8192, 192, 128, 2, 0, 1, pfd, 1);
+        snprintf(nm, sizeof nm, "mlp1 1cta TN192 S4 tiled pf%d", pfd); run<0, 4, 192>(nm, W, wrows, X, 2048, 8192, 192, 128, 2, 0, 1, pfd);
+        snprintf(nm, sizeof nm, "mlp1 cg2 TN192 S5 tiled pf%d", pfd); run<2, 5, 192>(nm, W, wrows, X, 2048, 8192, 192, 128, 2, 0, 1, pfd);
+        snprintf(nm, sizeof nm, "qkv 1cta TN128 S5 tiled pf%d", pfd); run<0, 5, 128>(nm, W, wrows, X, 2048, 3072, 128, 144, 2, 0, 1, pfd);
     }
     } else {
     // per-SM ingress vs grid size and stages (no MMA): is the limit per SM or per chip?
