@@ -74,7 +74,7 @@ bool mk_usable(const Ctx& c) {
     // default: the persistent kernel; ALPA_MK=0 selects the per-op kernel
     // sequence (A/B measurements and cross-checks)
     const char* e = getenv("ALPA_MK");
-    if ((e && e[0] == '0') || !c.bf16() || c.uniform_prefix < 0 || !c.tm_pre_valid) return false;
+    if ((e && e[0] == '0') || !c.bf16() || !c.tm_pre_valid) return false;
     const int64_t hd = c.kv() / c.cfg.heads;
     return hd == 64 || hd == 128;
 }
@@ -255,8 +255,12 @@ void mk_prepare(Ctx& c, int64_t n) {
         push(op, tag, 2.0 * M * L.in * L.out);
     };
     const int64_t pre_block = 2 * r * kv * 2;
+    // mixed per-lane prefixes (multi topology): one query tile per lane, prefix
+    // rows from the device lane map at run time
+    const bool multi = c.uniform_prefix < 0;
+    const int64_t upre = multi ? 0 : c.uniform_prefix;
     auto prefix_of = [&](int64_t b) {
-        return (const void*)((const uint8_t*)c.prefix + (c.uniform_prefix * B + b) * pre_block);
+        return (const void*)((const uint8_t*)c.prefix + (upre * B + b) * pre_block);
     };
 
     {
@@ -271,7 +275,8 @@ void mk_prepare(Ctx& c, int64_t n) {
     gemm(c.mlp2, menc2, c.ws.h1, EPI_F32, c.ws.e, ah, true, false, c.blocks[0].qkv.w, wb(c.blocks[0].qkv),
          "gemm_enc_mlp2", 5);
     std::vector<std::pair<int, int>> attn_part_maps;  // (map index, splits)
-    const int qtiles = (int)((M + 127) / 128);
+    const int qtiles = multi ? (int)n : (int)((M + 127) / 128);
+    const int prows = multi ? (int)n * 128 : (int)M;  // KV-split partial rows per split
     const int nbp = (int)((r + 63) / 64);
     for (int64_t b = 0; b < B; ++b) {
         const Block& blk = c.blocks[b];
@@ -284,6 +289,9 @@ void mk_prepare(Ctx& c, int64_t n) {
             op.tiles_t = qtiles;
             const int tiles = (int)H * qtiles;
             const int nbt_min = nbp + 1;
+            op.multi = multi ? 1 : 0;
+            op.blk = (int)b;
+            op.prows = prows;
             int smax = 6;  // attn_fixup merges at most 6 partials
             if (const char* e = getenv("ALPA_MK_ATTN_S")) smax = std::max(1, std::min(6, atoi(e)));
             op.splits = tiles >= G ? 1 : std::max(1, std::min({G / tiles, nbt_min, smax}));
@@ -295,7 +303,7 @@ void mk_prepare(Ctx& c, int64_t n) {
             op.tmX = dm(mq64);
             op.tmQ = dm(mq128);
             op.out = c.ws.ctxb;
-            const int64_t blkrow = (c.uniform_prefix * B + b) * 2;
+            const int64_t blkrow = (upre * B + b) * 2;
             op.pre_k_row = blkrow * r;
             op.pre_v_row = (blkrow + 1) * r;
             op.pf_ptr = blk.o.w;
@@ -308,8 +316,8 @@ void mk_prepare(Ctx& c, int64_t n) {
                 attn_part_maps.push_back({mp, op.splits});
                 op.tmXs = dm(mp);
             }
-            ws_floats = std::max(ws_floats, (size_t)op.splits * M * kv);
-            wsml_elems = std::max(wsml_elems, (size_t)op.splits * M * H);
+            ws_floats = std::max(ws_floats, (size_t)op.splits * prows * kv);
+            wsml_elems = std::max(wsml_elems, (size_t)op.splits * prows * H);
             push(op, "attention", 4.0 * n * A * (r + A) * kv);
         }
         gemm(blk.o, mblk[b * 4 + 1], c.ws.ctxb, EPI_RESID_F32, c.ws.e, ah, true, false, blk.mlp1.w,
@@ -333,8 +341,8 @@ void mk_prepare(Ctx& c, int64_t n) {
     m.ws = (float*)c.dalloc(ws_floats * sizeof(float));
     m.wsml = (float2*)c.dalloc(wsml_elems * sizeof(float2));
     for (auto& pm : attn_part_maps)
-        make_tmap_f32_3d_sw128(&maps[pm.first], m.ws, (uint64_t)kv, (uint64_t)M, (uint64_t)pm.second,
-                               (uint64_t)kv * 4, (uint64_t)M * kv * 4, 128);
+        make_tmap_f32_3d_sw128(&maps[pm.first], m.ws, (uint64_t)kv, (uint64_t)prows, (uint64_t)pm.second,
+                               (uint64_t)kv * 4, (uint64_t)prows * kv * 4, 128);
     m.d_maps = (CUtensorMap*)c.dalloc(maps.size() * sizeof(CUtensorMap));
     ALPA_CUDA(cudaMemcpy(m.d_maps, maps.data(), maps.size() * sizeof(CUtensorMap), cudaMemcpyHostToDevice));
     auto fix = [&](const CUtensorMap*& t) {
@@ -405,6 +413,8 @@ void mk_enqueue(Ctx& c, int64_t n, cudaStream_t s, unsigned long long* tstamp,
     p.H = (int)c.cfg.heads;
     p.r = (int)c.prefix_r;
     p.nft = (int)(c.ah() / 128);
+    p.B = (int)c.cfg.decoder_blocks;
+    p.lane_map = c.ws.lane_map;
     p.alpha = 1.0f / sqrtf((float)(c.kv() / c.cfg.heads));
     p.update_scale = c.cfg.update_scale;
     p.actions = c.ws.actions;

@@ -75,6 +75,11 @@ struct Op {
     const void* pf_ptr;      // bytes to pull into L2 while this op runs (a later op's weights)
     long long pf_bytes;
     long long pre_k_row, pre_v_row;  // attention: rows of this block's K / V in the prefix map
+    // attention, multi topology (per-lane prefixes, pipeline.cpp:405-413): one
+    // query tile per lane (rows 64..127 of the 128-row MMA tile are padding),
+    // the lane's prefix K/V at rows ((lane_map[lane] * B + blk) * 2 [+1]) * r
+    int multi, blk;
+    int prows;               // attention: rows of the KV-split partial workspace per split
 };
 
 struct Params {
@@ -85,6 +90,8 @@ struct Params {
     float* ws;        // split partials (fp32)
     float2* wsml;     // attention (m, l) partials
     int M, ah, kv, H, r, nft;
+    int B;                  // decoder blocks (prefix row arithmetic, multi topology)
+    const int* lane_map;    // [N] prefix index per lane (multi topology)
     float alpha, update_scale;
     float* actions;   // [M][2]
     const float* w_in;
@@ -272,6 +279,8 @@ __device__ inline GemmItem gemm_item(const Op& op, int it, int TN) {
 }
 struct AttnItem {
     int h, qt, s, tile, row0, g0, nj;
+    int rv;     // valid query rows of the 128-row tile
+    int prow0;  // first row of the tile in the KV-split partial workspace
 };
 __device__ inline AttnItem attn_item(const Op& op, int it, int M) {
     AttnItem a;
@@ -279,8 +288,11 @@ __device__ inline AttnItem attn_item(const Op& op, int it, int M) {
     a.tile = it / op.splits;
     a.h = a.tile % op.tiles_f;
     a.qt = a.tile / op.tiles_f;
-    a.row0 = a.qt * 128;
-    const int lanes = (M - a.row0) / 64 < 2 ? (M - a.row0) / 64 : 2;
+    // shared prefix: a tile = two lanes (128 rows); multi topology: one lane
+    a.row0 = op.multi ? a.qt * 64 : a.qt * 128;
+    a.rv = op.multi ? 64 : (M - a.row0 < 128 ? M - a.row0 : 128);
+    a.prow0 = op.multi ? a.qt * 128 : a.row0;
+    const int lanes = a.rv / 64;
     const int nbt = op.nbp + lanes;
     a.g0 = (a.s * nbt) / op.splits;
     a.nj = ((a.s + 1) * nbt) / op.splits - a.g0;
@@ -336,11 +348,12 @@ __device__ inline void attn_fixup(const Params& p, const Op& op, const AttnItem&
             const int idx = base + et + k * 256;
             const bool ok = idx < items;
             const int t = rb + idx / NQ, d = (idx % NQ) * 4;
+            const int pr = a.prow0 + (t - a.row0);  // partial workspace row
 #pragma unroll
             for (int q = 0; q < 6; ++q) {
                 const bool on = ok && q < np;
-                ml[k][q] = on ? __ldcg(p.wsml + ((int64_t)q * p.M + t) * p.H + a.h) : make_float2(-INFINITY, 0.f);
-                v[k][q] = on ? ldcg4(p.ws + ((int64_t)q * p.M + t) * p.kv + a.h * HD + d) : make_float4(0.f, 0.f, 0.f, 0.f);
+                ml[k][q] = on ? __ldcg(p.wsml + ((int64_t)q * op.prows + pr) * p.H + a.h) : make_float2(-INFINITY, 0.f);
+                v[k][q] = on ? ldcg4(p.ws + ((int64_t)q * op.prows + pr) * p.kv + a.h * HD + d) : make_float4(0.f, 0.f, 0.f, 0.f);
             }
         }
 #pragma unroll
@@ -797,6 +810,12 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                     bool waited = false;
                     for (int it = blockIdx.x; it < op.n_items; it += gridDim.x) {
                         const AttnItem a = attn_item(op, it, p.M);
+                        // this tile's prefix K / V rows (multi topology: the lane's own prefix)
+                        long long pre_k = op.pre_k_row, pre_v = op.pre_v_row;
+                        if (op.multi) {
+                            pre_k = ((long long)p.lane_map[a.qt] * p.B + op.blk) * 2 * p.r;
+                            pre_v = pre_k + p.r;
+                        }
                         auto load_block = [&](int j) {
                             const uint32_t st = (ks + j) % C::STAGES;
                             uint8_t* kb = slot_acquire(ks + j);
@@ -808,9 +827,9 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                                 const int col = a.h * HD + pn * 64;
                                 if (gb < op.nbp) {
                                     tma_load_2d_hint(kb + pn * C::KPANEL, op.tmW, &full[st], col,
-                                                     (int)(op.pre_k_row + gb * 64), ppol);
+                                                     (int)(pre_k + gb * 64), ppol);
                                     tma_load_2d_hint(vb + pn * C::KPANEL, op.tmW, &full[st], col,
-                                                     (int)(op.pre_v_row + gb * 64), ppol);
+                                                     (int)(pre_v + gb * 64), ppol);
                                 } else {
                                     const int row = a.row0 + (gb - op.nbp) * 64;
                                     tma_load_2d(kb + pn * C::KPANEL, op.tmX, &full[st], p.kv + col, row);
@@ -827,8 +846,8 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                             for (int j = pre; j < a.nj && a.g0 + j < op.nbp; ++j)
 #pragma unroll 1
                                 for (int pn = 0; pn < HD / 64; ++pn) {
-                                    tma_prefetch_box_2d(op.tmW, a.h * HD + pn * 64, (int)(op.pre_k_row + (a.g0 + j) * 64));
-                                    tma_prefetch_box_2d(op.tmW, a.h * HD + pn * 64, (int)(op.pre_v_row + (a.g0 + j) * 64));
+                                    tma_prefetch_box_2d(op.tmW, a.h * HD + pn * 64, (int)(pre_k + (a.g0 + j) * 64));
+                                    tma_prefetch_box_2d(op.tmW, a.h * HD + pn * 64, (int)(pre_v + (a.g0 + j) * 64));
                                 }
                         }
                         trace_ev<TR>(p, o, TR_PRE);
@@ -1290,6 +1309,7 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                         int hi = 32;
                         if (gb < op.nbp) hi = min(32, p.r - gb * 64 - hh * 32);
                         else if ((i >> 6) != gb - op.nbp) hi = 0;
+                        if (i >= a.rv) hi = 0;  // padding rows (multi topology, ragged tail)
                         const float* srf = reinterpret_cast<const float*>(sr);
                         // block max of the raw scores (tree: no 32-deep dependency chain);
                         // max(s) * scale == max(s * scale) for scale > 0
@@ -1407,7 +1427,7 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                         for (int e2 = 0; e2 < 16; ++e2)
                             v[e2] = (w0 * __uint_as_float(oa[e2]) + w1 * __uint_as_float(ob[e2])) * sc;
                         if (final_out) {
-                            if (t < p.M) {
+                            if (i < a.rv) {
                                 __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(op.out) + (int64_t)t * p.kv + a.h * HD + hh * DH + cc;
 #pragma unroll
                                 for (int e2 = 0; e2 < 16; e2 += 4)
@@ -1427,13 +1447,14 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                                 fence_proxy_async();
                                 asm volatile("bar.sync %0, 128;" ::"r"(3 + hh) : "memory");
                                 if (q == 0 && lane == 0) {
-                                    tma_store_3d(op.tmXs, pst + (d0 >> 5) * (128 * 128), a.h * HD + (d0 & ~31), a.row0, a.s);
+                                    tma_store_3d(op.tmXs, pst + (d0 >> 5) * (128 * 128), a.h * HD + (d0 & ~31), a.prow0, a.s);
                                     bulk_commit();
                                 }
                             }
                         }
                     }
-                    if (hh == 0 && t < p.M && !final_out) p.wsml[((int64_t)a.s * p.M + t) * p.H + a.h] = make_float2(mm, lsum);
+                    if (hh == 0 && i < a.rv && !final_out)
+                        p.wsml[((int64_t)a.s * op.prows + a.prow0 + i) * p.H + a.h] = make_float2(mm, lsum);
                     if (!final_out && (et & 127) == 0) {  // the two panel-store issuers
                         bulk_wait_all();
                         fence_proxy_async_global();
@@ -1445,8 +1466,9 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                     ++nmma;
                     if (!final_out) {
                         split_meet<TR>(p, op, o, p.splitc + op.split_base + a.tile, et);
-                        const int rb = a.row0 + (a.s * 128) / op.splits;
-                        const int re = min(p.M, a.row0 + ((a.s + 1) * 128) / op.splits);
+                        const int R = op.multi ? 64 : 128;
+                        const int rb = a.row0 + (a.s * R) / op.splits;
+                        const int re = min(a.row0 + a.rv, a.row0 + ((a.s + 1) * R) / op.splits);
                         attn_fixup<HD>(p, op, a, rb, re, et);
                     }
                     publish<TR>(p, o, et);

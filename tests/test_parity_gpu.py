@@ -309,6 +309,72 @@ def test_persistent_kernel_vs_per_op_path(port, monkeypatch, n, B, K, r):
     assert rel_l2(out["1"], out["0"]) <= BF16_TOL
 
 
+@pytest.mark.parametrize("n,B,K,r,lane_map", [(3, 2, 2, 300, None), (5, 1, 2, 130, [2, 0, 2, 1, 0])])
+def test_persistent_kernel_multi_topology(port, monkeypatch, n, B, K, r, lane_map):
+    """Multi topology (lane l attends prefix lane_map[l], pipeline.cpp:405-413)
+    on the persistent kernel: one query tile per lane, the lane's prefix rows
+    read from the device lane map.  Within the bf16 bar of the oracle, equal
+    to the per-op path within the bar, graph == eager bitwise, and one
+    persistent launch per iteration (the persistent kernel really ran)."""
+    m = c2(B=B, K=K)
+    npre = 3 if lane_map else n
+    pre = np.stack([port.synthetic_prefix(500 + 100 * l, B, r, m.kv_dim) for l in range(npre)])
+    lp = np.array(lane_map if lane_map else list(range(n)), np.int32)
+    exp = port.refine(ocfg(m), port.weights(ocfg(m)), pre, port.noise(2, 1, n), lane_prefix=lp)
+    out = {}
+    for mk in ("1", "0"):
+        monkeypatch.setenv("ALPA_MK", mk)
+        with alpa.ActionGenerator(m) as g:
+            g.bind_prefix(pre)
+            if lane_map:
+                g.set_lane_prefix(lp)
+            req = alpa.InferenceRequest(num_trajectories=n, topology="multi", v0=5.0)
+            res = g.run_action_generation(req)
+            res_e = g.run_action_generation(alpa.InferenceRequest(num_trajectories=n, topology="multi",
+                                                                  v0=5.0, executor="eager"))
+        np.testing.assert_array_equal(res.actions, res_e.actions)
+        if mk == "1":
+            assert res.stats["kernel_launches"] == K + 1
+        out[mk] = res.actions
+        err = rel_l2(res.actions, exp)
+        print(f"multi ALPA_MK={mk} n={n} B={B} K={K} r={r} map={lp.tolist()}: rel-L2 {err:.3e}")
+        assert err <= BF16_TOL
+    assert rel_l2(out["1"], out["0"]) <= BF16_TOL
+
+
+@pytest.mark.parametrize("topology", ["single", "multi"])
+def test_bf16_compare_actiongen_variants(port, topology):
+    """cmd_compare_actiongen (cli.cpp:236-313) on the bf16 tensor-core path:
+    the reference's three variants (baseline = dynamic KV + eager, +static_kv,
+    +graph) produce bitwise-equal actions (cli.cpp:292-300), for the shared
+    prefix and for per-lane prefixes; graph + dynamic is a ConfigError
+    (model.cpp:609-611)."""
+    m = c2(B=2, K=2)
+    n, r = 4, 200
+    if topology == "single":
+        pre = port.synthetic_prefix(4242, 2, r, m.kv_dim)
+    else:
+        pre = np.stack([port.synthetic_prefix(900 + l, 2, r, m.kv_dim) for l in range(n)])
+    variants = {"baseline": ("dynamic", "eager"), "+static_kv": ("static", "eager"),
+                "+graph": ("static", "graph")}
+    got = {}
+    with alpa.ActionGenerator(m) as g:
+        g.bind_prefix(pre)
+        for name, (kv, ex) in variants.items():
+            res = g.run_action_generation(alpa.InferenceRequest(
+                num_trajectories=n, topology=topology, kv_strategy=kv, executor=ex, v0=5.0))
+            got[name] = res
+        with pytest.raises(alpa.ConfigError):
+            g.run_action_generation(alpa.InferenceRequest(num_trajectories=n, topology=topology,
+                                                          kv_strategy="dynamic", executor="graph"))
+    for name in variants:
+        np.testing.assert_array_equal(got[name].actions, got["baseline"].actions)
+        np.testing.assert_array_equal(got[name].trajectories, got["baseline"].trajectories)
+    lp = None if topology == "single" else np.arange(n, dtype=np.int32)
+    exp = port.refine(ocfg(m), port.weights(ocfg(m)), pre, port.noise(2, 1, n), lane_prefix=lp)
+    assert rel_l2(got["baseline"].actions, exp) <= BF16_TOL
+
+
 def test_persistent_kernel_single_launch_per_iteration(port):
     """One persistent launch per denoising iteration (+ the rollout)."""
     m = c2(B=2, K=3, action_hidden_dim=256, kv_dim=128, heads=1)
