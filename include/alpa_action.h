@@ -147,6 +147,34 @@ int alpa_prefix_device(alpa_ctx* ctx, void** ptr, int64_t* bytes);
 /* Multi topology: lane l attends prefix lane_map[l] (default: all 0). */
 int alpa_set_lane_prefix(alpa_ctx* ctx, const int32_t* lane_map, int64_t n);
 
+/* ---- reasoning-stage KV producer --------------------------
+ * The language model's prefill / decode on the device, writing every token's
+ * K/V in place into a static-capacity buffer in the action stage's prefix
+ * layout [lanes][B][2][capacity][kv] (context dtype); seal binds it as the
+ * prefix with no copy.  The caller keeps the vision encoder, the tokenizer and
+ * the sampler loop, like Engine::reasoning_pass (pipeline.cpp:247-390). */
+/* KvCache(static) with reasoning_capacity = T + max_new_tokens
+ * (pipeline.cpp:281-288); lanes = 1 (single topology) or N (multi). Unbinds a
+ * prefix the context produced earlier. */
+int alpa_reasoning_begin(alpa_ctx* ctx, int64_t lanes, int64_t capacity);
+/* Model::prefill (model.cpp:408-464) over ctx = [vision rows | prompt
+ * embeddings] + positions (pipeline.cpp:297-325): vision_rows [lanes][P][hidden]
+ * host f32 (may be NULL when P == 0), prompt_ids [n_prompt]; then
+ * logits_head (model.cpp:509-513): logits_out [lanes][vocab] host. */
+int alpa_reasoning_prefill(alpa_ctx* ctx, const float* vision_rows, int64_t P,
+                           const int64_t* prompt_ids, int64_t n_prompt, float* logits_out);
+/* One decode step (pipeline.cpp:368-386, Model::decode_step model.cpp:484-507):
+ * token_ids [lanes] at the next position, K/V appended, logits_out [lanes][vocab]. */
+int alpa_reasoning_decode(alpa_ctx* ctx, const int64_t* token_ids, float* logits_out);
+/* KvCache::seal_reasoning (kv_cache.cpp:181-190): bind the produced KV as the
+ * action stage's prefix (n_prefix = lanes, r = tokens appended, in place). */
+int alpa_reasoning_seal(alpa_ctx* ctx, int64_t* r_out);
+/* sample_token (model.cpp:30-54) on the host, bit-exact: greedy argmax, or
+ * the temperature-1 softmax CDF walk in double with the Rng state (splitmix64,
+ * common.hpp:36-59) advanced in place; InternalError on NaN logits. */
+int alpa_sample_token(const float* logits, int64_t vocab, int stochastic, uint64_t* rng_state,
+                      int64_t* token_out);
+
 /* ---- the path ----------------------------------------------------------- */
 /* Host in, host out: host noise (bit-exact Rng::normal) -> H2D -> K-step
  * refine (one CUDA graph) -> device rollout -> D2H.  actions_out [N][64][2],

@@ -239,6 +239,9 @@ class Ref:
                                             C.c_int, _f32p, C.POINTER(C.c_double),
                                             C.POINTER(C.c_int64), C.POINTER(C.c_double)]
         L.ref_rollout.argtypes = [_f32p, C.c_int64, C.c_float, _f32p]
+        _i64p = C.POINTER(C.c_int64)
+        L.ref_reasoning_io.argtypes = [C.POINTER(Cfg), C.c_char_p, C.c_uint64, C.c_int, _f32p, C.c_int64,
+                                       _i64p, _i64p, C.c_int64, _i64p, _i64p, C.c_int64, _i64p, _i64p]
         L.ref_action_weights.argtypes = [C.POINTER(Cfg), C.c_int, _f32p, C.c_int64,
                                          C.POINTER(C.c_int64)]
         L.ref_parse_latency_report.argtypes = [C.c_char_p, C.POINTER(C.c_int64), C.POINTER(C.c_double)]
@@ -279,6 +282,22 @@ class Ref:
                                                  C.byref(kvb), C.byref(it)))
         self.last_iter_ms = float(it.value)  # sum of DiffusionResult::iter_ms
         return out, float(ms.value), int(kvb.value)
+
+    def reasoning_io(self, cfg: Cfg, scenario: str, sampler_seed=1, stochastic=True):
+        """(vision rows [P][hidden], prompt ids, decode-loop ids, T, m) of the
+        reference's reasoning stage on a scenario (ref_reasoning_io)."""
+        i64 = lambda a: a.ctypes.data_as(C.POINTER(C.c_int64))
+        P, npr, m, T = C.c_int64(), C.c_int64(), C.c_int64(), C.c_int64()
+        self._check(self.L.ref_reasoning_io(C.byref(cfg), scenario.encode(), sampler_seed, int(stochastic),
+                                            None, 0, C.byref(P), None, 0, C.byref(npr), None, 0,
+                                            C.byref(m), C.byref(T)))
+        vis = np.empty((P.value, cfg.hidden_dim), np.float32)
+        prompt = np.empty(npr.value, np.int64)
+        ids = np.empty(max(m.value, 1), np.int64)
+        self._check(self.L.ref_reasoning_io(C.byref(cfg), scenario.encode(), sampler_seed, int(stochastic),
+                                            _fp(vis), vis.size, C.byref(P), i64(prompt), prompt.size,
+                                            C.byref(npr), i64(ids), ids.size, C.byref(m), C.byref(T)))
+        return vis, prompt, ids[: m.value], int(T.value), int(m.value)
 
     def rollout(self, actions: np.ndarray, v0: float) -> np.ndarray:
         actions = np.ascontiguousarray(actions, np.float32)

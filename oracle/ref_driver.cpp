@@ -140,6 +140,62 @@ int ref_scenario_prefix(const RefCfg* c, const char* scenario_path,
     });
 }
 
+// Inputs and outputs of the reasoning stage on a scenario (single topology),
+// for the device KV producer's parity test: the vision encoder's rows
+// (Model::vision_encode, model.cpp:326-392, on the request's patch rows as in
+// pipeline.cpp:265-277) [P][hidden], the prompt token ids
+// (Engine::preprocess), and the ids the decode loop fed back
+// (Engine::run_reasoning: cot tokens, plus the terminator when the loop
+// stopped on it, pipeline.cpp:345-386); T = P + prompt, m = decode steps.
+// Null outputs: size query.
+int ref_reasoning_io(const RefCfg* c, const char* scenario_path, std::uint64_t sampler_seed,
+                     int stochastic, float* vision_out, std::int64_t vision_cap,
+                     std::int64_t* P_out, std::int64_t* prompt_out, std::int64_t prompt_cap,
+                     std::int64_t* n_prompt_out, std::int64_t* ids_out, std::int64_t ids_cap,
+                     std::int64_t* m_out, std::int64_t* T_out) {
+    return guarded([&] {
+        const ModelConfig cfg = to_cfg(c);
+        Engine engine(cfg);
+        RunConfig rc;
+        rc.model = cfg;
+        const Scenario sc = load_scenario(scenario_path);
+        InferenceRequest req = request_from_scenario(sc, rc);
+        req.topology = Topology::Single;
+        req.num_trajectories = 1;
+        req.kv_strategy = KvStrategy::Static;
+        req.executor = ExecMode::Eager;
+        req.sampler_seed = sampler_seed;
+        req.sampler_mode = stochastic ? SampleMode::Stochastic : SampleMode::Greedy;
+        const Engine::Preprocessed pre = engine.preprocess(req);
+        Substrate& sub = engine.substrate();
+        const BufferId patch = sub.alloc({pre.patches, pre.patch_dim});
+        sub.write(patch, pre.patch_rows);
+        const BufferId vis = engine.model().vision_encode(patch, 1, pre.patches);
+        const auto v = sub.read(vis);
+        const std::int64_t np = static_cast<std::int64_t>(pre.prompt.ids.size());
+        ReasoningOutput ro = engine.run_reasoning(req);
+        std::vector<std::int64_t> ids = ro.cot_tokens[0];
+        if (static_cast<std::int64_t>(ids.size()) < ro.token_count)
+            ids.push_back(engine.tokenizer().termination_token());
+        if (P_out) *P_out = pre.patches;
+        if (n_prompt_out) *n_prompt_out = np;
+        if (m_out) *m_out = ro.token_count;
+        if (T_out) *T_out = pre.patches + np;
+        if (vision_out) {
+            if (vision_cap < static_cast<std::int64_t>(v.size())) throw InternalError("vision buffer too small");
+            std::memcpy(vision_out, v.data(), v.size() * sizeof(float));
+        }
+        if (prompt_out) {
+            if (prompt_cap < np) throw InternalError("prompt buffer too small");
+            for (std::int64_t i = 0; i < np; ++i) prompt_out[i] = pre.prompt.ids[i];
+        }
+        if (ids_out) {
+            if (ids_cap < static_cast<std::int64_t>(ids.size())) throw InternalError("ids buffer too small");
+            for (std::size_t i = 0; i < ids.size(); ++i) ids_out[i] = ids[i];
+        }
+    });
+}
+
 // Engine::run_action_generation on a batch-1 prefix [B][2][r][kv] f32.
 // topology_single: 1 = Single (replicate_for_batch when n>1); 0 = Multi
 // (prefix replicated by the caller into batch n: prefix is [B][2][n][r][kv]).

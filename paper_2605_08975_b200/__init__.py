@@ -144,8 +144,24 @@ def lib():
                                           _f64p, _f64p]
         L.alpa_eval_open_loop_device.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                                  C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]
+        _i64p = C.POINTER(C.c_int64)
+        L.alpa_reasoning_begin.argtypes = [C.c_void_p, C.c_int64, C.c_int64]
+        L.alpa_reasoning_prefill.argtypes = [C.c_void_p, _f32p, C.c_int64, _i64p, C.c_int64, _f32p]
+        L.alpa_reasoning_decode.argtypes = [C.c_void_p, _i64p, _f32p]
+        L.alpa_reasoning_seal.argtypes = [C.c_void_p, _i64p]
+        L.alpa_sample_token.argtypes = [_f32p, C.c_int64, C.c_int, C.POINTER(C.c_uint64), _i64p]
         _lib = L
     return _lib
+
+
+def sample_token(logits: np.ndarray, stochastic: bool, state: int) -> tuple[int, int]:
+    """minivla::sample_token (model.cpp:30-54), host, bit-exact: returns
+    (token, advanced Rng state)."""
+    lg = np.ascontiguousarray(logits, np.float32)
+    st = C.c_uint64(state)
+    tok = C.c_int64()
+    _check(lib().alpa_sample_token(_fp(lg), lg.size, int(stochastic), C.byref(st), C.byref(tok)))
+    return int(tok.value), int(st.value)
 
 
 def _check(rc: int, ctx=None) -> None:
@@ -290,6 +306,81 @@ class ActionGenerator:
         m = np.ascontiguousarray(lane_map, np.int32)
         _check(lib().alpa_set_lane_prefix(self._h, m.ctypes.data_as(C.POINTER(C.c_int32)),
                                           m.size), self._h)
+
+    # -- reasoning-stage KV producer ------------------------------
+    def reasoning_begin(self, lanes: int, capacity: int) -> None:
+        """Static in-place KV of `capacity` tokens per lane (T + max_new_tokens,
+        pipeline.cpp:281-286) in the action stage's prefix layout."""
+        _check(lib().alpa_reasoning_begin(self._h, lanes, capacity), self._h)
+
+    def reasoning_prefill(self, vision: np.ndarray, prompt_ids, lanes: int = 1) -> np.ndarray:
+        """Model::prefill over [vision rows | prompt embeddings] + positions;
+        vision [P][h] (shared by every lane) or [lanes][P][h]. Returns logits
+        [lanes][vocab]."""
+        v = np.ascontiguousarray(vision, np.float32)
+        if v.ndim == 2:
+            v = np.ascontiguousarray(np.broadcast_to(v, (lanes,) + v.shape))
+        ids = np.ascontiguousarray(prompt_ids, np.int64)
+        out = np.empty((v.shape[0], self.cfg.vocab_size), np.float32)
+        _check(lib().alpa_reasoning_prefill(self._h, _fp(v), v.shape[1],
+                                            ids.ctypes.data_as(C.POINTER(C.c_int64)), ids.size,
+                                            _fp(out)), self._h)
+        return out
+
+    def reasoning_decode(self, ids) -> np.ndarray:
+        """One decode step: ids [lanes] at the next position. Returns logits."""
+        t = np.ascontiguousarray(ids, np.int64)
+        out = np.empty((t.size, self.cfg.vocab_size), np.float32)
+        _check(lib().alpa_reasoning_decode(self._h, t.ctypes.data_as(C.POINTER(C.c_int64)), _fp(out)),
+               self._h)
+        return out
+
+    def reasoning_seal(self) -> int:
+        """KvCache::seal_reasoning: the produced KV becomes the action prefix in place."""
+        r = C.c_int64()
+        _check(lib().alpa_reasoning_seal(self._h, C.byref(r)), self._h)
+        return int(r.value)
+
+    def run_reasoning(self, vision: np.ndarray, prompt_ids, lanes: int = 1, max_new_tokens: int = 256,
+                      sampler_seed: int = 1, stochastic: bool = True, forced_cot_tokens: int = 0,
+                      termination_token: int = 0, forced_ids=None) -> dict:
+        """Engine::reasoning_pass (pipeline.cpp:279-390) around the device
+        producer: prefill, then the decode loop with the reference's host
+        sampler (per-lane Rng(sampler_seed + lane)), then seal.  forced_ids
+        [m][lanes] teacher-forces the fed-back ids instead of sampling.
+        Returns {cot_tokens, token_count, r, prompt_tokens}."""
+        v = np.asarray(vision, np.float32)
+        T = v.shape[-2] + len(prompt_ids)
+        self.reasoning_begin(lanes, T + max_new_tokens)
+        logits = self.reasoning_prefill(v, prompt_ids, lanes)
+        states = [sampler_seed + l for l in range(lanes)]
+        done = [False] * lanes
+        cot = [[] for _ in range(lanes)]
+        forced = forced_cot_tokens > 0
+        max_m = min(forced_cot_tokens, max_new_tokens) if forced else max_new_tokens
+        m = 0
+        while m < max_m:
+            if all(done) and not forced:
+                break
+            if forced_ids is not None:
+                if m >= len(forced_ids):
+                    break
+                ids = [int(x) for x in np.atleast_1d(forced_ids[m])]
+            else:
+                ids = []
+                for l in range(lanes):
+                    tok, states[l] = sample_token(logits[l], stochastic, states[l])
+                    ids.append(tok)
+            for l in range(lanes):
+                if not done[l]:
+                    if not forced and ids[l] == termination_token:
+                        done[l] = True
+                    else:
+                        cot[l].append(ids[l])
+            m += 1
+            logits = self.reasoning_decode(ids)
+        r = self.reasoning_seal()
+        return {"cot_tokens": cot, "token_count": m, "r": r, "prompt_tokens": T}
 
     def set_stream(self, stream_handle: int) -> None:
         _check(lib().alpa_set_stream(self._h, C.c_void_p(stream_handle)), self._h)

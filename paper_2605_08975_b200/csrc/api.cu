@@ -388,6 +388,7 @@ int alpa_bind_prefix_device(alpa_ctx* h, const void* kv, int64_t n_prefix, int64
         c->own_prefix = false;
         c->prefix_n = n_prefix;
         c->prefix_r = r;
+        c->prefix_cap = r;
         alpa::refresh_prefix_map(*c);
         alpa::invalidate_graph(*c);
     });
@@ -418,7 +419,81 @@ int alpa_prefix_device(alpa_ctx* h, void** ptr, int64_t* bytes) {
         if (!c || !ptr || !bytes) fail(ALPA_ERR_CONFIG, "null argument");
         if (!c->prefix) fail(ALPA_ERR_INTERNAL, "no prefix bound");
         *ptr = c->prefix;
-        *bytes = c->prefix_n * c->cfg.decoder_blocks * 2 * c->prefix_r * c->kv() * (int64_t)c->esz();
+        *bytes = c->prefix_n * c->cfg.decoder_blocks * 2 * c->pcap() * c->kv() * (int64_t)c->esz();
+    });
+}
+
+// ---------------------------------------------------------------- reasoning producer
+int alpa_reasoning_begin(alpa_ctx* h, int64_t lanes, int64_t capacity) {
+    Ctx* c = reinterpret_cast<Ctx*>(h);
+    return guarded(c, [&] {
+        if (!c) fail(ALPA_ERR_CONFIG, "null context");
+        cudaSetDevice(c->device);
+        alpa::reasoning_begin(*c, lanes, capacity);
+    });
+}
+
+int alpa_reasoning_prefill(alpa_ctx* h, const float* vision_rows, int64_t P, const int64_t* prompt_ids,
+                           int64_t n_prompt, float* logits_out) {
+    Ctx* c = reinterpret_cast<Ctx*>(h);
+    return guarded(c, [&] {
+        if (!c) fail(ALPA_ERR_CONFIG, "null context");
+        if (P < 0 || n_prompt < 0) fail(ALPA_ERR_CONFIG, "negative token count");
+        cudaSetDevice(c->device);
+        alpa::reasoning_prefill(*c, vision_rows, P, prompt_ids, n_prompt, logits_out);
+    });
+}
+
+int alpa_reasoning_decode(alpa_ctx* h, const int64_t* token_ids, float* logits_out) {
+    Ctx* c = reinterpret_cast<Ctx*>(h);
+    return guarded(c, [&] {
+        if (!c) fail(ALPA_ERR_CONFIG, "null context");
+        cudaSetDevice(c->device);
+        alpa::reasoning_decode(*c, token_ids, logits_out);
+    });
+}
+
+int alpa_reasoning_seal(alpa_ctx* h, int64_t* r_out) {
+    Ctx* c = reinterpret_cast<Ctx*>(h);
+    return guarded(c, [&] {
+        if (!c) fail(ALPA_ERR_CONFIG, "null context");
+        cudaSetDevice(c->device);
+        const int64_t r = alpa::reasoning_seal(*c);
+        if (r_out) *r_out = r;
+    });
+}
+
+int alpa_sample_token(const float* logits, int64_t vocab, int stochastic, uint64_t* rng_state,
+                      int64_t* token_out) {
+    // host logic only (no context): error text via alpa_last_error(NULL)
+    return guarded(nullptr, [&] {
+        if (!logits || !token_out || (stochastic && !rng_state)) fail(ALPA_ERR_CONFIG, "null argument");
+        if (vocab < 1) fail(ALPA_ERR_INTERNAL, "sample_token: empty logits");
+        for (int64_t i = 0; i < vocab; ++i)
+            if (std::isnan(logits[i])) fail(ALPA_ERR_INTERNAL, "sample_token: NaN logits");
+        if (!stochastic) {
+            int64_t best = 0;
+            for (int64_t i = 1; i < vocab; ++i)
+                if (logits[i] > logits[best]) best = i;
+            *token_out = best;
+            return;
+        }
+        double mx = logits[0];
+        for (int64_t i = 0; i < vocab; ++i) mx = std::max(mx, static_cast<double>(logits[i]));
+        double sum = 0.0;
+        for (int64_t i = 0; i < vocab; ++i) sum += std::exp(static_cast<double>(logits[i]) - mx);
+        HostRng rng{*rng_state};
+        const double u = static_cast<double>(rng.next_float()) * sum;
+        *rng_state = rng.s;
+        double acc = 0.0;
+        for (int64_t i = 0; i < vocab; ++i) {
+            acc += std::exp(static_cast<double>(logits[i]) - mx);
+            if (u < acc) {
+                *token_out = i;
+                return;
+            }
+        }
+        *token_out = vocab - 1;
     });
 }
 

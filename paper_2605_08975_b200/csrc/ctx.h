@@ -77,7 +77,7 @@ struct KInfo {
 // completion / split counters and the split-partial workspace.
 struct MkState {
     bool valid = false;
-    int64_t n = -1, uniform = -2, r = -1, prefix_n = -1;
+    int64_t n = -1, uniform = -2, r = -1, cap = -1, prefix_n = -1;
     const void* prefix = nullptr;
     void* d_ops = nullptr;
     int n_ops = 0;
@@ -108,6 +108,27 @@ struct GraphCache {
     int64_t nodes = 0;
 };
 
+// Reasoning-stage language model: reference-layout f32 weights
+// ([in][out] + bias, model.cpp:72-101) and the static in-place KV it produces.
+struct LangBlock {
+    float *wq, *bq, *wk, *bk, *wv, *bv, *wo, *bo, *w1, *b1, *w2, *b2;
+};
+struct Reasoner {
+    bool weights = false;
+    std::vector<LangBlock> blocks;
+    float *embed = nullptr, *lm_w = nullptr, *lm_b = nullptr;  // token_embed [V][h], lm_head
+    int64_t lanes = 0, cap = 0, T = 0, len = 0;  // len: tokens appended per lane
+    bool open = false;                 // begun, not sealed
+    void* kv = nullptr;                // [lanes][B][2][cap][kv] in the context dtype (the action prefix)
+    float* kv32 = nullptr;             // f32 working copy for the LM's own attention (bf16 contexts)
+    float* pos = nullptr;              // [cap + 1][h] sinusoid (pipeline.cpp:291-295)
+    float *x = nullptr, *xn = nullptr, *q = nullptr, *k = nullptr, *v = nullptr, *att = nullptr,
+          *h1 = nullptr, *last = nullptr, *logits = nullptr;
+    int32_t* ids = nullptr;            // [lanes] decode tokens / [n_prompt] prompt ids
+    int64_t rows_cap = 0, ids_cap = 0;
+    std::vector<void*> bufs;           // per-begin allocations
+};
+
 struct Ctx {
     alpa_model_cfg cfg{};
     int device = 0;
@@ -121,16 +142,22 @@ struct Ctx {
     float* pos = nullptr;  // [64][ah] sinusoid (model.cpp:56-68)
     std::vector<void*> allocations;
 
-    void* prefix = nullptr;  // [n_prefix][B][2][r][kv] f32 or bf16
+    void* prefix = nullptr;  // [n_prefix][B][2][cap][kv] f32 or bf16, tokens [0, r) valid
     bool own_prefix = false;
     int64_t prefix_n = 0, prefix_r = 0;
+    // rows per K / V section: the static reasoning capacity when the prefix
+    // was produced in place on the device (KvLayout::reasoning_capacity,
+    // pipeline.cpp:281-286), else r
+    int64_t prefix_cap = 0;
+    int64_t pcap() const { return prefix_cap > 0 ? prefix_cap : prefix_r; }
     std::vector<int32_t> lane_map_host;  // multi topology
     int64_t uniform_prefix = 0;          // prefix index shared by every lane, -1 if mixed
-    CUtensorMap tm_pre{};                // 2-D view [n_prefix*B*2*r][kv], box {64, 128}
+    CUtensorMap tm_pre{};                // 2-D view [n_prefix*B*2*cap][kv], box {64, 128}
     bool tm_pre_valid = false;
 
     Workspace ws;
     MkState mk;
+    Reasoner rs;
     std::vector<ProfSpan> prof_spans;
     GraphCache graph;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
@@ -170,6 +197,16 @@ void make_prefix_synthetic(Ctx& c, uint64_t seed, int64_t r);
 void synthesize_prefix_into(Ctx& c, void* dst, uint64_t seed, int64_t r);
 void make_prefix_from_host(Ctx& c, const float* host, int64_t n_prefix, int64_t r);
 int64_t stream_offset(const alpa_model_cfg& c);
+// one f32 [in][out] linear (w then b) / a flat array drawn from the weight stream at `base`
+void draw_linear_f32(Ctx& c, int64_t base, int64_t in, int64_t out, float* w, float* b);
+void draw_array_f32(Ctx& c, int64_t base, int64_t n, float* dst);
+// reasoning-stage KV producer (reason.cu)
+void reasoning_begin(Ctx& c, int64_t lanes, int64_t capacity);
+void reasoning_prefill(Ctx& c, const float* vision_rows, int64_t P, const int64_t* prompt_ids,
+                       int64_t n_prompt, float* logits_out);
+void reasoning_decode(Ctx& c, const int64_t* ids, float* logits_out);
+int64_t reasoning_seal(Ctx& c);
+void reasoning_release(Ctx& c);
 int64_t param_count(const alpa_model_cfg& c);
 
 // path.cu

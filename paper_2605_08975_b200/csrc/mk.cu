@@ -90,7 +90,7 @@ void mk_release(Ctx& c) {
 void mk_prepare(Ctx& c, int64_t n) {
     MkState& m = c.mk;
     if (m.valid && m.n == n && m.prefix == c.prefix && m.uniform == c.uniform_prefix &&
-        m.r == c.prefix_r && m.prefix_n == c.prefix_n)
+        m.r == c.prefix_r && m.cap == c.pcap() && m.prefix_n == c.prefix_n)
         return;
     mk_release(c);
     const int G = num_sms(c);
@@ -138,7 +138,7 @@ void mk_prepare(Ctx& c, int64_t n) {
     CUtensorMap t64{};
     make_tmap_bf16_2d(&t64, c.ws.qkv, 3 * kv, M, 3 * kv * 2, 64, 64);
     const int mq64 = add_map(t64);
-    const uint64_t pre_rows = (uint64_t)c.prefix_n * B * 2 * r;
+    const uint64_t pre_rows = (uint64_t)c.prefix_n * B * 2 * c.pcap();
     make_tmap_bf16_2d(&t64, c.prefix, (uint64_t)kv, pre_rows, (uint64_t)kv * 2, 64, 64);
     const int mpre = add_map(t64);
     const int menc1 = add_map(c.mlp1.tmap), menc2 = add_map(c.mlp2.tmap);
@@ -254,7 +254,8 @@ void mk_prepare(Ctx& c, int64_t n) {
         if (op.splits > 1) ws_floats = std::max(ws_floats, (size_t)tiles * op.splits * ttn * 128);
         push(op, tag, 2.0 * M * L.in * L.out);
     };
-    const int64_t pre_block = 2 * r * kv * 2;
+    const int64_t pcap = c.pcap();  // rows per K / V section of the prefix
+    const int64_t pre_block = 2 * pcap * kv * 2;
     // mixed per-lane prefixes (multi topology): one query tile per lane, prefix
     // rows from the device lane map at run time
     const bool multi = c.uniform_prefix < 0;
@@ -304,8 +305,8 @@ void mk_prepare(Ctx& c, int64_t n) {
             op.tmQ = dm(mq128);
             op.out = c.ws.ctxb;
             const int64_t blkrow = (upre * B + b) * 2;
-            op.pre_k_row = blkrow * r;
-            op.pre_v_row = (blkrow + 1) * r;
+            op.pre_k_row = blkrow * pcap;
+            op.pre_v_row = (blkrow + 1) * pcap;
             op.pf_ptr = blk.o.w;
             op.pf_bytes = (pf_mask >> 6) & 1 ? wb(blk.o) : 0;
             if (op.splits > 1) {
@@ -392,6 +393,7 @@ void mk_prepare(Ctx& c, int64_t n) {
     m.prefix = c.prefix;
     m.uniform = c.uniform_prefix;
     m.r = r;
+    m.cap = c.pcap();
     m.prefix_n = c.prefix_n;
     m.valid = true;
 }
@@ -412,6 +414,7 @@ void mk_enqueue(Ctx& c, int64_t n, cudaStream_t s, unsigned long long* tstamp,
     p.kv = (int)c.kv();
     p.H = (int)c.cfg.heads;
     p.r = (int)c.prefix_r;
+    p.rcap = (int)c.pcap();
     p.nft = (int)(c.ah() / 128);
     p.B = (int)c.cfg.decoder_blocks;
     p.lane_map = c.ws.lane_map;

@@ -91,6 +91,7 @@ struct Params {
     float2* wsml;     // attention (m, l) partials
     int M, ah, kv, H, r, nft;
     int B;                  // decoder blocks (prefix row arithmetic, multi topology)
+    int rcap;               // prefix rows per K / V section (static capacity >= r)
     const int* lane_map;    // [N] prefix index per lane (multi topology)
     float alpha, update_scale;
     float* actions;   // [M][2]
@@ -813,8 +814,8 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                         // this tile's prefix K / V rows (multi topology: the lane's own prefix)
                         long long pre_k = op.pre_k_row, pre_v = op.pre_v_row;
                         if (op.multi) {
-                            pre_k = ((long long)p.lane_map[a.qt] * p.B + op.blk) * 2 * p.r;
-                            pre_v = pre_k + p.r;
+                            pre_k = ((long long)p.lane_map[a.qt] * p.B + op.blk) * 2 * p.rcap;
+                            pre_v = pre_k + p.rcap;
                         }
                         auto load_block = [&](int j) {
                             const uint32_t st = (ks + j) % C::STAGES;

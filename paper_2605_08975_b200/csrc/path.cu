@@ -215,7 +215,7 @@ template <typename T>
 __global__ void __launch_bounds__(256)
     attn_simt_kernel(const T* __restrict__ qkv, const T* __restrict__ prefix,
                      int64_t prefix_stride, int64_t block_off, const int32_t* __restrict__ lane_map,
-                     int n, int r, int kv, int H, int A, float alpha, T* __restrict__ ctx) {
+                     int n, int r, int cap, int kv, int H, int A, float alpha, T* __restrict__ ctx) {
     pdl_wait();
     pdl_launch();
     __shared__ float qs[8][128];
@@ -229,7 +229,7 @@ __global__ void __launch_bounds__(256)
     for (int d = lane; d < hd; d += 32) qs[warp][d] = to_f(qrow[d]);
     __syncwarp();
     const T* pk = prefix + lane_map[l] * prefix_stride + block_off + h * hd;
-    const T* pv = pk + (int64_t)r * kv;
+    const T* pv = pk + (int64_t)cap * kv;  // V section: cap rows after K (static capacity)
     const T* ak = qkv + (int64_t)l * A * ld + kv + h * hd;
     const T* av = ak + kv;
     const int Ttot = r + A;
@@ -558,8 +558,8 @@ void launch_attn(Ctx& c, const KInfo& info, int64_t n, int64_t b, cudaStream_t s
     if (const char* e = getenv("ALPA_ATTN_SPLITS")) S = std::max(1, std::min(atoi(e), a.nbp + 1));
     a.splits = S;
     const int64_t blk = (c.uniform_prefix * c.cfg.decoder_blocks + b) * 2;
-    a.pre_k_row = blk * r;
-    a.pre_v_row = (blk + 1) * r;
+    a.pre_k_row = blk * c.pcap();
+    a.pre_v_row = (blk + 1) * c.pcap();
     a.alpha = 1.0f / sqrtf((float)(kv / H));
     a.ctx = (__nv_bfloat16*)c.ws.ctxb;
     a.pf_ptr = pf;
@@ -654,8 +654,8 @@ void enqueue_iteration(Ctx& c, int64_t n, cudaStream_t s) {
     Workspace& w = c.ws;
     const int64_t A = c.steps(), M = n * A, ah = c.ah(), kv = c.kv(), H = c.cfg.heads;
     const int T = (int)M;
-    const int64_t r = c.prefix_r;
-    const int64_t prefix_stride = c.cfg.decoder_blocks * 2 * r * kv;
+    const int64_t r = c.prefix_r, cap = c.pcap();
+    const int64_t prefix_stride = c.cfg.decoder_blocks * 2 * cap * kv;
     const float alpha = 1.0f / sqrtf((float)(kv / H));
     const int ln_grid = (int)((M + 7) / 8);
     const int attn_grid = (int)((n * H * A + 7) / 8);
@@ -685,7 +685,7 @@ void enqueue_iteration(Ctx& c, int64_t n, cudaStream_t s) {
             sd.pf_bytes = nb;
             return sd;
         };
-        const int64_t pre_block = 2 * r * kv * 2;  // K + V of one block, bf16
+        const int64_t pre_block = 2 * cap * kv * 2;  // K + V of one block, bf16
         auto prefix_of = [&](int64_t b) {
             return (const void*)((const uint8_t*)c.prefix +
                                  (c.uniform_prefix < 0 ? 0 : c.uniform_prefix) *
@@ -708,8 +708,8 @@ void enqueue_iteration(Ctx& c, int64_t n, cudaStream_t s) {
                     launch_attn<64>(c, att, n, b, s, blk.o.w, wbytes(blk.o));
             } else {
                 launch(c, att, attn_simt_kernel<bf>, dim3(attn_grid), dim3(256), 0, s,
-                       (const bf*)w.qkv, (const bf*)c.prefix, prefix_stride, b * 2 * r * kv,
-                       (const int32_t*)w.lane_map, (int)n, (int)r, (int)kv, (int)H, (int)A,
+                       (const bf*)w.qkv, (const bf*)c.prefix, prefix_stride, b * 2 * cap * kv,
+                       (const int32_t*)w.lane_map, (int)n, (int)r, (int)cap, (int)kv, (int)H, (int)A,
                        alpha, (bf*)w.ctxb);
             }
             gemm_tc<EPI_RESID_F32>(c, "gemm_o", blk.o, w.tm_ctx, T, w.e, ah, s,
@@ -734,8 +734,8 @@ void enqueue_iteration(Ctx& c, int64_t n, cudaStream_t s) {
                    (const float*)w.e, x, M, ah);
             gemm_f32<EPI_F32>(c, "gemm_qkv", blk.qkv, x, ah, T, (float*)w.qkv, 3 * kv, s);
             launch(c, att, attn_simt_kernel<float>, dim3(attn_grid), dim3(256), 0, s,
-                   (const float*)w.qkv, (const float*)c.prefix, prefix_stride, b * 2 * r * kv,
-                   (const int32_t*)w.lane_map, (int)n, (int)r, (int)kv, (int)H, (int)A, alpha,
+                   (const float*)w.qkv, (const float*)c.prefix, prefix_stride, b * 2 * cap * kv,
+                   (const int32_t*)w.lane_map, (int)n, (int)r, (int)cap, (int)kv, (int)H, (int)A, alpha,
                    (float*)w.ctxb);
             gemm_f32<EPI_RESID_F32>(c, "gemm_o", blk.o, (const float*)w.ctxb, kv, T, w.e, ah, s);
             launch(c, ln, layernorm_kernel<float>, dim3(ln_grid), dim3(256), 0, s,
@@ -760,7 +760,7 @@ void enqueue_rollout(Ctx& c, int64_t n, const float* d_actions, float* d_traj, c
 void refresh_prefix_map(Ctx& c) {
     c.tm_pre_valid = false;
     if (!c.bf16() || !c.prefix) return;
-    const uint64_t rows = (uint64_t)c.prefix_n * c.cfg.decoder_blocks * 2 * c.prefix_r;
+    const uint64_t rows = (uint64_t)c.prefix_n * c.cfg.decoder_blocks * 2 * c.pcap();
     make_tmap_bf16_2d(&c.tm_pre, c.prefix, (uint64_t)c.kv(), rows, (uint64_t)c.kv() * 2, 64, 128);
     c.tm_pre_valid = true;
 }

@@ -119,6 +119,19 @@ inline int grid_for(int64_t n) {
 
 }  // namespace
 
+void draw_linear_f32(Ctx& c, int64_t base, int64_t in, int64_t out, float* w, float* b) {
+    Src src{nullptr, c.cfg.weight_seed, 0};
+    place_weight_f32<<<grid_for(in * out), 256, 0, c.stream>>>(src, base, in, out, w, out, 0);
+    place_bias<<<grid_for(out), 256, 0, c.stream>>>(src, base + in * out, out, b, 0);
+    ALPA_CUDA(cudaGetLastError());
+}
+
+void draw_array_f32(Ctx& c, int64_t base, int64_t n, float* dst) {
+    Src src{nullptr, c.cfg.weight_seed, 0};
+    place_bias<<<grid_for(n), 256, 0, c.stream>>>(src, base, n, dst, 0);
+    ALPA_CUDA(cudaGetLastError());
+}
+
 void load_weights(Ctx& c, const float* host_arena, int64_t count, uint64_t seed, int64_t offset) {
     const alpa_model_cfg& cfg = c.cfg;
     const int64_t ah = cfg.action_hidden_dim, kv = cfg.kv_dim, B = cfg.decoder_blocks;
@@ -251,6 +264,7 @@ void make_prefix_synthetic(Ctx& c, uint64_t seed, int64_t r) {
     ALPA_CUDA(cudaStreamSynchronize(c.stream));
     c.prefix_n = 1;
     c.prefix_r = r;
+    c.prefix_cap = r;
     refresh_prefix_map(c);
 }
 
@@ -274,6 +288,7 @@ void make_prefix_from_host(Ctx& c, const float* host, int64_t n_prefix, int64_t 
     }
     c.prefix_n = n_prefix;
     c.prefix_r = r;
+    c.prefix_cap = r;
     refresh_prefix_map(c);
 }
 

@@ -87,3 +87,42 @@ def test_no_cpu_fallback_without_gpu():
         pytest.skip("GPU present")
     with pytest.raises(alpa.InternalError, match="no CUDA device"):
         alpa.ActionGenerator(alpa.ModelConfig())
+
+
+def test_host_sampler_matches_restatement():
+    """alpa_sample_token (host, no GPU): sample_token (model.cpp:30-54) --
+    greedy argmax, and the temperature-1 CDF walk in double over
+    Rng::next_float (splitmix64 >> 40, common.hpp:36-59)."""
+    import math
+
+    def splitmix(state):
+        state = (state + 0x9E3779B97F4A7C15) & (2**64 - 1)
+        z = state
+        z = ((z ^ (z >> 30)) * 0xBF58476D1CE4E5B9) & (2**64 - 1)
+        z = ((z ^ (z >> 27)) * 0x94D049BB133111EB) & (2**64 - 1)
+        return state, z ^ (z >> 31)
+
+    def ref_sample(lg, state):
+        mx = max(float(v) for v in lg)
+        tot = sum(math.exp(float(v) - mx) for v in lg)
+        state, z = splitmix(state)
+        u = float(np.float32(z >> 40) * np.float32(1.0 / 16777216.0)) * tot
+        acc = 0.0
+        for i, v in enumerate(lg):
+            acc += math.exp(float(v) - mx)
+            if u < acc:
+                return i, state
+        return len(lg) - 1, state
+
+    rng = np.random.default_rng(7)
+    state = 1
+    for _ in range(50):
+        lg = (rng.standard_normal(512) * 3).astype(np.float32)
+        tok, st = alpa.sample_token(lg, True, state)
+        assert (tok, st) == ref_sample(lg, state)
+        state = st
+        assert alpa.sample_token(lg, False, 0)[0] == int(np.argmax(lg))
+    bad = np.zeros(8, np.float32)
+    bad[3] = np.nan
+    with pytest.raises(alpa.InternalError):
+        alpa.sample_token(bad, True, 1)
