@@ -104,6 +104,15 @@ public:
         const std::int64_t eff = (request.topology == minivla::Topology::Single && n > 1) ? n : batch;
         if (eff != n) throw minivla::InternalError("kv batch does not match the requested trajectory count");
         bind(sub, kv);
+        std::vector<minivla::ActionSequence> out = generate(request, diff, kv_bytes);
+        return out;
+    }
+
+private:
+    std::vector<minivla::ActionSequence> generate(const minivla::InferenceRequest& request,
+                                                  minivla::Model::DiffusionResult* diff = nullptr,
+                                                  std::int64_t* kv_bytes = nullptr) {
+        const std::int64_t n = request.num_trajectories;
         alpa_request r{};
         r.num_trajectories = n;
         r.lane0 = 0;
@@ -137,6 +146,7 @@ public:
         return out;
     }
 
+public:
     // actions_to_trajectory (pipeline.cpp:124-148) on the device, bit-exact
     // with the reference's fp64 host loop; throws InternalError like it.
     minivla::Trajectory actions_to_trajectory(const minivla::ActionSequence& a, float initial_speed) {
@@ -154,6 +164,82 @@ public:
     }
 
     const alpa_stats& last_stats() const { return last_; }
+
+    // Engine::run_reasoning with the KV produced ON THE DEVICE:
+    // the reference engine keeps the vision encoder and the tokenizer
+    // (Engine::preprocess, Model::vision_encode on the lane-tiled patch rows,
+    // pipeline.cpp:265-277); the language model's prefill / decode run in the
+    // library and append K/V in place into the action stage's layout
+    // (static capacity T + max_new_tokens, pipeline.cpp:281-286); the decode
+    // loop is reasoning_pass's (pipeline.cpp:330-388) with the reference's
+    // sampler (alpa_sample_token, bit-exact).  The sealed KV stays bound in the
+    // library: run_action_generation_device() then attends it with no copy.
+    struct DeviceReasoning {
+        std::vector<std::vector<std::int64_t>> cot_tokens;  // per lane, no terminator
+        std::int64_t token_count = 0;                       // decode steps executed
+        std::int64_t prompt_tokens = 0;                     // T
+        std::int64_t reasoning_len = 0;                     // r = T + token_count
+    };
+    DeviceReasoning run_reasoning(minivla::Engine& engine, const minivla::InferenceRequest& request) {
+        minivla::Engine::validate_request(request);
+        const minivla::ModelConfig& m = engine.config();
+        const std::int64_t lanes = request.topology == minivla::Topology::Multi ? request.num_trajectories : 1;
+        const minivla::Engine::Preprocessed pre = engine.preprocess(request);
+        minivla::Substrate& sub = engine.substrate();
+        const std::int64_t P = pre.patches, h = m.hidden_dim, V = m.vocab_size;
+        std::vector<float> tiled(static_cast<size_t>(lanes * P * pre.patch_dim));
+        for (std::int64_t l = 0; l < lanes; ++l)
+            std::copy(pre.patch_rows.begin(), pre.patch_rows.end(), tiled.begin() + l * P * pre.patch_dim);
+        const std::size_t mark = sub.alloc_mark();
+        const minivla::BufferId patch = sub.alloc({lanes * P, pre.patch_dim});
+        sub.write(patch, tiled);
+        const minivla::BufferId vis = engine.model().vision_encode(patch, lanes, P);
+        const auto vrows = sub.read(vis);
+        std::vector<float> vision(vrows.begin(), vrows.end());  // [lanes][P][h]
+        sub.free_allocated_since(mark);
+        const std::vector<std::int64_t>& prompt = pre.prompt.ids;
+        const std::int64_t T = P + static_cast<std::int64_t>(prompt.size());
+        check(alpa_reasoning_begin(ctx_, lanes, T + m.max_new_tokens), ctx_);
+        std::vector<float> logits(static_cast<size_t>(lanes * V));
+        check(alpa_reasoning_prefill(ctx_, vision.data(), P, prompt.data(), static_cast<std::int64_t>(prompt.size()),
+                                     logits.data()),
+              ctx_);
+        DeviceReasoning out;
+        out.cot_tokens.assign(static_cast<size_t>(lanes), {});
+        out.prompt_tokens = T;
+        std::vector<std::uint64_t> rng(static_cast<size_t>(lanes));
+        for (std::int64_t l = 0; l < lanes; ++l) rng[l] = request.sampler_seed + static_cast<std::uint64_t>(l);
+        std::vector<bool> done(static_cast<size_t>(lanes), false);
+        const bool forced = request.forced_cot_tokens > 0;
+        const std::int64_t max_m = forced ? std::min(request.forced_cot_tokens, m.max_new_tokens) : m.max_new_tokens;
+        const int stochastic = request.sampler_mode == minivla::SampleMode::Stochastic ? 1 : 0;
+        const std::int64_t term = engine.tokenizer().termination_token();
+        std::vector<std::int64_t> ids(static_cast<size_t>(lanes));
+        std::int64_t steps = 0;
+        while (steps < max_m) {
+            bool all_done = true;
+            for (std::int64_t l = 0; l < lanes; ++l) all_done = all_done && done[l];
+            if (all_done && !forced) break;
+            for (std::int64_t l = 0; l < lanes; ++l) {
+                check(alpa_sample_token(logits.data() + l * V, V, stochastic, &rng[l], &ids[l]), nullptr);
+                if (!done[l]) {
+                    if (!forced && ids[l] == term) done[l] = true;
+                    else out.cot_tokens[l].push_back(ids[l]);
+                }
+            }
+            steps += 1;
+            check(alpa_reasoning_decode(ctx_, ids.data(), logits.data()), ctx_);
+        }
+        out.token_count = steps;
+        check(alpa_reasoning_seal(ctx_, &out.reasoning_len), ctx_);
+        (void)h;
+        return out;
+    }
+
+    // Engine::run_action_generation on the KV run_reasoning left on the device.
+    std::vector<minivla::ActionSequence> run_action_generation_device(const minivla::InferenceRequest& request) {
+        return generate(request);
+    }
 
 private:
     // Pack the sealed reasoning tokens of every block / lane into

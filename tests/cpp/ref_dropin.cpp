@@ -13,6 +13,10 @@
 // to the first (cli.cpp:292-300), kv_bytes == LatencyReport::kv_bytes, and the
 // reference's error types for N = 0 and graph + dynamic.
 //
+// Plus the reasoning stage on the device (ActionStage::run_reasoning, SURVEY
+// §8f-1): chain-of-thought tokens equal to Engine::run_reasoning's, and
+// actions / trajectories off the in-place device KV vs Engine::infer.
+//
 // Prints one JSON line per case; exit 0 all pass, 3 a failure (cli.cpp:528-540).
 #include <cmath>
 #include <cstdio>
@@ -130,6 +134,37 @@ int main(int argc, char** argv) {
                         rollout_bitexact ? "true" : "false", same ? "true" : "false", (long long)kvb,
                         (long long)ref.latency.kv_bytes, pass ? "true" : "false");
                 }
+            }
+        }
+        // the reasoning stage on the device: the reference engine keeps
+        // vision + tokenizer; the LM's prefill/decode and the KV run in the library and
+        // the action stage attends the KV in place -- vs Engine::infer end to end
+        for (Topology topo : {Topology::Single, Topology::Multi}) {
+            for (std::int64_t n : {1, 6}) {
+                RunConfig c = rc;
+                c.topology = topo;
+                c.num_trajectories = n;
+                c.kv_strategy = KvStrategy::Static;
+                c.executor = ExecMode::Graph;
+                InferenceRequest req = request_from_scenario(sc, c);
+                const InferenceResult ref = engine.infer(req);
+                ReasoningOutput refr = engine.run_reasoning(req);
+                const auto dr = gpu.run_reasoning(engine, req);
+                const auto acts = gpu.run_action_generation_device(req);
+                const float v0 = initial_speed_from_history(req.pose_history);
+                std::vector<Trajectory> traj;
+                for (const auto& a : acts) traj.push_back(actions_to_trajectory(a, v0));
+                const double ea = rel_l2(flat(acts), flat(ref.actions));
+                const double et = rel_l2(flat(traj), flat(ref.trajectories));
+                const bool tokens_equal = dr.cot_tokens == refr.cot_tokens && dr.token_count == refr.token_count;
+                const bool len_equal = dr.reasoning_len == refr.kv.reasoning_len();
+                const bool pass = ea <= 1e-4 && et <= 1e-4 && tokens_equal && len_equal;
+                ok = ok && pass;
+                std::printf(
+                    "{\"device_reasoning\": true, \"topology\": \"%s\", \"n\": %lld, \"r\": %lld, "
+                    "\"tokens_equal\": %s, \"rel_l2_actions\": %.3e, \"rel_l2_traj\": %.3e, \"pass\": %s}\n",
+                    topo == Topology::Single ? "single" : "multi", (long long)n, (long long)dr.reasoning_len,
+                    tokens_equal ? "true" : "false", ea, et, pass ? "true" : "false");
             }
         }
         // the reference's error types through the adapter

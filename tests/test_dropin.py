@@ -41,5 +41,7 @@ def test_reference_engine_with_gpu_action_stage():
     assert out.returncode == 0, out.stderr + out.stdout
     cases = [l for l in lines if "variant" in l]
     errors = [l for l in lines if "error_case" in l]
+    reasoning = [l for l in lines if l.get("device_reasoning")]
     assert len(cases) == 12 and all(c["pass"] for c in cases)
     assert len(errors) == 3 and all(e["pass"] for e in errors)
+    assert len(reasoning) == 4 and all(c["pass"] for c in reasoning)
