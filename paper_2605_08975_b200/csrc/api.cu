@@ -308,6 +308,10 @@ void alpa_ctx_destroy(alpa_ctx* h) {
     cudaSetDevice(c->device);
     if (c->stream) cudaStreamSynchronize(c->stream);
     if (c->graph.exec) cudaGraphExecDestroy(c->graph.exec);
+    try {
+        alpa::reasoning_release(*c);  // decode-step graph, pinned slots
+    } catch (...) {
+    }
     for (void* p : c->allocations) cudaFree(p);
     if (c->pinned) cudaFreeHost(c->pinned);
     if (c->ev0) cudaEventDestroy(c->ev0);

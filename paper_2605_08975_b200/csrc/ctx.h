@@ -126,6 +126,10 @@ struct Reasoner {
           *h1 = nullptr, *last = nullptr, *logits = nullptr;
     int32_t* ids = nullptr;            // [lanes] decode tokens / [n_prompt] prompt ids
     int64_t rows_cap = 0, ids_cap = 0;
+    int64_t* dlen = nullptr;           // device cache length (position of the next token)
+    int32_t* h_ids = nullptr;          // pinned [lanes]: the step graph's input ids
+    float* h_logits = nullptr;         // pinned [lanes][vocab]: the step graph's output
+    cudaGraphExec_t step = nullptr;    // one captured decode step, replayed per token
     std::vector<void*> bufs;           // per-begin allocations
 };
 

@@ -39,7 +39,8 @@ int64_t blk_n(int64_t w, int64_t kv) {
 __global__ void rs_embed_rows(const float* __restrict__ table, const int32_t* __restrict__ ids,
                               const float* __restrict__ rows_in, const float* __restrict__ pos,
                               int64_t n, int h, int64_t p0, int64_t pstep, int64_t ldx, int64_t x_off,
-                              float* __restrict__ x) {
+                              float* __restrict__ x, const int64_t* __restrict__ dpos) {
+    if (dpos) p0 += *dpos;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n * h;
          e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t t = e / h;
@@ -94,7 +95,8 @@ __global__ void rs_linear(const float* __restrict__ A, int64_t rows, int in, con
 template <typename T>
 __global__ void rs_append(const float* __restrict__ k, const float* __restrict__ v, int64_t n, int lanes,
                           int64_t pos0, int64_t B, int64_t b, int64_t cap, int kv, float* __restrict__ kv32,
-                          T* __restrict__ kvo) {
+                          T* __restrict__ kvo, const int64_t* __restrict__ dpos) {
+    if (dpos) pos0 += *dpos;
     const int64_t total = (int64_t)lanes * n * kv;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
          e += (int64_t)gridDim.x * blockDim.x) {
@@ -124,7 +126,8 @@ __global__ void rs_append(const float* __restrict__ k, const float* __restrict__
 // chunks, lane owns head dims lane + 32u.
 __global__ void rs_attention(const float* __restrict__ q, int64_t nq, int lanes, int64_t pos0,
                              const float* __restrict__ kv32, int64_t B, int64_t b, int64_t cap, int kv,
-                             int H, float alpha, float* __restrict__ ctx) {
+                             int H, float alpha, float* __restrict__ ctx, const int64_t* __restrict__ dpos) {
+    if (dpos) pos0 += *dpos;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t gw = blockIdx.x * (int64_t)(blockDim.x / 32) + warp;
     if (gw >= (int64_t)lanes * nq * H) return;
@@ -170,6 +173,10 @@ __global__ void rs_attention(const float* __restrict__ q, int64_t nq, int lanes,
         const int d = lane + 32 * u;
         if (d < hd) orow[d] = o[u] * inv;
     }
+}
+
+__global__ void rs_bump(int64_t* dpos, int64_t by) {
+    if (threadIdx.x == 0 && blockIdx.x == 0) *dpos += by;
 }
 
 // last row of every lane -> out (ReadSlice, model.cpp:454-463)
@@ -251,7 +258,9 @@ void ensure_ids(Ctx& c, int64_t n) {
 // The language blocks over n new positions [pos0, pos0 + n) of every lane
 // (rows = lanes * n in R.x), appending their K/V, then LN_f of each lane's
 // last row and the logits head (model.cpp:429-464, 484-513).
-void lm_forward(Ctx& c, int64_t n, int64_t pos0, float* logits_out) {
+// dpos: device position added to pos0 (decode: the graph-captured step reads the
+// cache length from the device, so one captured step serves every token)
+void lm_forward(Ctx& c, int64_t n, int64_t pos0, const int64_t* dpos) {
     Reasoner& R = c.rs;
     const alpa_model_cfg& m = c.cfg;
     const int64_t h = m.hidden_dim, kv = m.kv_dim, V = m.vocab_size, B = m.decoder_blocks, H = m.heads;
@@ -269,12 +278,12 @@ void lm_forward(Ctx& c, int64_t n, int64_t pos0, float* logits_out) {
         rs_linear<RS_PLAIN><<<grid_of(rows * kv), 256, 0, s>>>(R.xn, rows, (int)h, W.wv, W.bv, (int)kv, R.v);
         if (c.bf16())
             rs_append<__nv_bfloat16><<<grid_of(rows * kv), 256, 0, s>>>(
-                R.k, R.v, n, L, pos0, B, b, R.cap, (int)kv, R.kv32, (__nv_bfloat16*)R.kv);
+                R.k, R.v, n, L, pos0, B, b, R.cap, (int)kv, R.kv32, (__nv_bfloat16*)R.kv, dpos);
         else
             rs_append<float><<<grid_of(rows * kv), 256, 0, s>>>(R.k, R.v, n, L, pos0, B, b, R.cap, (int)kv,
-                                                                nullptr, (float*)R.kv);
+                                                                nullptr, (float*)R.kv, dpos);
         rs_attention<<<(int)((rows * H + 7) / 8), 256, 0, s>>>(R.q, n, L, pos0, kv32, B, b, R.cap, (int)kv,
-                                                               (int)H, alpha, R.att);
+                                                               (int)H, alpha, R.att, dpos);
         rs_linear<RS_RESID><<<grid_of(rows * h), 256, 0, s>>>(R.att, rows, (int)kv, W.wo, W.bo, (int)h, R.x);
         rs_layernorm<<<ln_grid, 256, 0, s>>>(R.x, R.xn, rows, (int)h);
         rs_linear<RS_GELU><<<grid_of(rows * 4 * h), 256, 0, s>>>(R.xn, rows, (int)h, W.w1, W.b1, (int)(4 * h), R.h1);
@@ -285,15 +294,18 @@ void lm_forward(Ctx& c, int64_t n, int64_t pos0, float* logits_out) {
     rs_last_rows<<<grid_of(L * h), 256, 0, s>>>(R.xn, n, L, (int)h, R.last);
     rs_linear<RS_PLAIN><<<grid_of(L * V), 256, 0, s>>>(R.last, L, (int)h, R.lm_w, R.lm_b, (int)V, R.logits);
     check_launch();
-    if (logits_out)
-        ALPA_CUDA(cudaMemcpyAsync(logits_out, R.logits, (size_t)L * V * sizeof(float), cudaMemcpyDeviceToHost, s));
-    ALPA_CUDA(cudaStreamSynchronize(s));
 }
 
 }  // namespace
 
 void reasoning_release(Ctx& c) {
     Reasoner& R = c.rs;
+    if (R.step) cudaGraphExecDestroy(R.step);
+    R.step = nullptr;
+    if (R.h_ids) cudaFreeHost(R.h_ids);
+    if (R.h_logits) cudaFreeHost(R.h_logits);
+    R.h_ids = nullptr;
+    R.h_logits = nullptr;
     for (void* p : R.bufs) c.dfree(p);
     R.bufs.clear();
     R.kv = nullptr;
@@ -340,6 +352,10 @@ void reasoning_begin(Ctx& c, int64_t lanes, int64_t capacity) {
     R.pos = (float*)c.dalloc(pos.size() * sizeof(float));
     R.bufs.push_back(R.pos);
     ALPA_CUDA(cudaMemcpyAsync(R.pos, pos.data(), pos.size() * sizeof(float), cudaMemcpyHostToDevice, c.stream));
+    R.dlen = (int64_t*)c.dalloc(sizeof(int64_t));
+    R.bufs.push_back(R.dlen);
+    ALPA_CUDA(cudaMallocHost(&R.h_ids, (size_t)lanes * sizeof(int32_t)));
+    ALPA_CUDA(cudaMallocHost(&R.h_logits, (size_t)lanes * m.vocab_size * sizeof(float)));
     R.last = (float*)c.dalloc((size_t)lanes * h * sizeof(float));
     R.logits = (float*)c.dalloc((size_t)lanes * m.vocab_size * sizeof(float));
     R.bufs.push_back(R.last);
@@ -378,13 +394,19 @@ void reasoning_prefill(Ctx& c, const float* vision_rows, int64_t P, const int64_
     for (int64_t l = 0; l < L; ++l) {
         if (P > 0)
             rs_embed_rows<<<grid_of(P * h), 256, 0, s>>>(nullptr, nullptr, vis + l * P * h, R.pos, P, (int)h, 0, 1,
-                                                          h, l * T * h, R.x);
+                                                          h, l * T * h, R.x, nullptr);
         if (n_prompt > 0)
             rs_embed_rows<<<grid_of(n_prompt * h), 256, 0, s>>>(R.embed, R.ids, nullptr, R.pos, n_prompt, (int)h, P,
-                                                                 1, h, (l * T + P) * h, R.x);
+                                                                 1, h, (l * T + P) * h, R.x, nullptr);
     }
     check_launch();
-    lm_forward(c, T, 0, logits_out);
+    lm_forward(c, T, 0, nullptr);
+    if (logits_out)
+        ALPA_CUDA(cudaMemcpyAsync(logits_out, R.logits, (size_t)L * c.cfg.vocab_size * sizeof(float),
+                                  cudaMemcpyDeviceToHost, s));
+    // the device cache length the captured decode step reads
+    ALPA_CUDA(cudaMemcpyAsync(R.dlen, &T, sizeof(int64_t), cudaMemcpyHostToDevice, s));
+    ALPA_CUDA(cudaStreamSynchronize(s));
     if (vis) c.dfree(vis);
     R.T = T;
     R.len = T;
@@ -396,20 +418,34 @@ void reasoning_decode(Ctx& c, const int64_t* ids, float* logits_out) {
     if (R.len + 1 > R.cap) fail(ALPA_ERR_INTERNAL, "decode workspace too small for cache length");
     if (!ids) fail(ALPA_ERR_CONFIG, "null token ids");
     const int64_t h = c.cfg.hidden_dim, V = c.cfg.vocab_size, L = R.lanes;
-    std::vector<int32_t> t((size_t)L);
     for (int64_t l = 0; l < L; ++l) {
         if (ids[l] < 0 || ids[l] >= V) fail(ALPA_ERR_CONFIG, "token id out of range");
-        t[l] = (int32_t)ids[l];
+        R.h_ids[l] = (int32_t)ids[l];
     }
-    ensure_rows(c, L);
-    ensure_ids(c, L);
     cudaStream_t s = c.stream;
-    ALPA_CUDA(cudaMemcpyAsync(R.ids, t.data(), L * sizeof(int32_t), cudaMemcpyHostToDevice, s));
-    // x = embed(id) + pos[T + m - 1] (pipeline.cpp:371-386): every lane's token sits
-    // at the next free row of the cache
-    rs_embed_rows<<<grid_of(L * h), 256, 0, s>>>(R.embed, R.ids, nullptr, R.pos, L, (int)h, R.len, 0, h, 0, R.x);
-    check_launch();
-    lm_forward(c, 1, R.len, logits_out);
+    if (!R.step) {
+        // One decode step (pipeline.cpp:371-386 + Model::decode_step + logits_head)
+        // captured once per begin and replayed per token: the ids come from a
+        // pinned host slot, the position (the cache length) from the device, and
+        // the step ends by advancing it -- one graph launch per token.
+        ensure_rows(c, L);
+        ensure_ids(c, L);
+        cudaGraph_t g = nullptr;
+        ALPA_CUDA(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal));
+        ALPA_CUDA(cudaMemcpyAsync(R.ids, R.h_ids, L * sizeof(int32_t), cudaMemcpyHostToDevice, s));
+        // x = embed(id) + pos[T + m - 1]: every lane's token sits at the next free row
+        rs_embed_rows<<<grid_of(L * h), 256, 0, s>>>(R.embed, R.ids, nullptr, R.pos, L, (int)h, 0, 0, h, 0, R.x,
+                                                      R.dlen);
+        lm_forward(c, 1, 0, R.dlen);
+        rs_bump<<<1, 32, 0, s>>>(R.dlen, 1);
+        ALPA_CUDA(cudaMemcpyAsync(R.h_logits, R.logits, (size_t)L * V * sizeof(float), cudaMemcpyDeviceToHost, s));
+        ALPA_CUDA(cudaStreamEndCapture(s, &g));
+        ALPA_CUDA(cudaGraphInstantiate(&R.step, g, 0));
+        cudaGraphDestroy(g);
+    }
+    ALPA_CUDA(cudaGraphLaunch(R.step, s));
+    ALPA_CUDA(cudaStreamSynchronize(s));
+    if (logits_out) std::memcpy(logits_out, R.h_logits, (size_t)L * V * sizeof(float));
     R.len += 1;
 }
 
