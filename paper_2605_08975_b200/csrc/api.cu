@@ -724,25 +724,18 @@ int alpa_eval_open_loop(alpa_ctx* h, const float* traj, const float* gt, int64_t
         const size_t tb = (size_t)(scenes * n * steps * 3) * sizeof(float);
         const size_t gb = gt ? (size_t)(scenes * steps * 3) * sizeof(float) : 0;
         const size_t ob = (size_t)scenes * sizeof(double);
-        uint8_t* d = nullptr;
-        ALPA_CUDA(cudaMalloc(&d, tb + gb + 2 * ob + 64));
+        uint8_t* d = static_cast<uint8_t*>(c->io(tb + gb + 2 * ob + 64));
         float* dt = reinterpret_cast<float*>(d);
         float* dg = gt ? reinterpret_cast<float*>(d + tb) : nullptr;
         double* dm = reinterpret_cast<double*>(d + ((tb + gb + 15) & ~(size_t)15));
         double* dv = dm + scenes;
-        try {
-            ALPA_CUDA(cudaMemcpyAsync(dt, traj, tb, cudaMemcpyHostToDevice, c->stream));
-            if (gt) ALPA_CUDA(cudaMemcpyAsync(dg, gt, gb, cudaMemcpyHostToDevice, c->stream));
-            alpa::eval_open_loop_device(*c, dt, dg, scenes, n, steps, min_ade ? dm : nullptr,
-                                        diversity ? dv : nullptr, c->stream);
-            if (min_ade) ALPA_CUDA(cudaMemcpyAsync(min_ade, dm, ob, cudaMemcpyDeviceToHost, c->stream));
-            if (diversity) ALPA_CUDA(cudaMemcpyAsync(diversity, dv, ob, cudaMemcpyDeviceToHost, c->stream));
-            ALPA_CUDA(cudaStreamSynchronize(c->stream));
-        } catch (...) {
-            cudaFree(d);
-            throw;
-        }
-        cudaFree(d);
+        ALPA_CUDA(cudaMemcpyAsync(dt, traj, tb, cudaMemcpyHostToDevice, c->stream));
+        if (gt) ALPA_CUDA(cudaMemcpyAsync(dg, gt, gb, cudaMemcpyHostToDevice, c->stream));
+        alpa::eval_open_loop_device(*c, dt, dg, scenes, n, steps, min_ade ? dm : nullptr,
+                                    diversity ? dv : nullptr, c->stream);
+        if (min_ade) ALPA_CUDA(cudaMemcpyAsync(min_ade, dm, ob, cudaMemcpyDeviceToHost, c->stream));
+        if (diversity) ALPA_CUDA(cudaMemcpyAsync(diversity, dv, ob, cudaMemcpyDeviceToHost, c->stream));
+        ALPA_CUDA(cudaStreamSynchronize(c->stream));
     });
 }
 
@@ -770,9 +763,8 @@ int alpa_rollout(alpa_ctx* h, const float* actions, int64_t n, float v0, float* 
         if (n < 1) return;
         cudaSetDevice(c->device);
         const int64_t A = c->steps();
-        float *da = nullptr, *dt = nullptr;
-        ALPA_CUDA(cudaMalloc(&da, n * A * 2 * sizeof(float)));
-        ALPA_CUDA(cudaMalloc(&dt, n * A * 3 * sizeof(float)));
+        float* da = static_cast<float*>(c->io((size_t)n * A * 5 * sizeof(float)));
+        float* dt = da + n * A * 2;
         ALPA_CUDA(cudaMemcpyAsync(da, actions, n * A * 2 * sizeof(float), cudaMemcpyHostToDevice,
                                   c->stream));
         ALPA_CUDA(cudaMemcpyAsync(c->d_scalars, &v0, sizeof(float), cudaMemcpyHostToDevice,
@@ -784,8 +776,6 @@ int alpa_rollout(alpa_ctx* h, const float* actions, int64_t n, float v0, float* 
         ALPA_CUDA(cudaMemcpyAsync(&hbad, c->d_scalars + 1, sizeof(int), cudaMemcpyDeviceToHost,
                                   c->stream));
         ALPA_CUDA(cudaStreamSynchronize(c->stream));
-        cudaFree(da);
-        cudaFree(dt);
         if (hbad) fail(ALPA_ERR_INTERNAL, "actions_to_trajectory: non-finite action");
     });
 }

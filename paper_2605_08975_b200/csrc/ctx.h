@@ -178,6 +178,16 @@ struct Ctx {
     size_t dev_bytes = 0;              // device bytes allocated by the context
     void* eval_scratch = nullptr;  // eval.cu: per-(scene, term) mean displacements
     size_t eval_scratch_bytes = 0;
+    void* io_scratch = nullptr;    // host-buffer entry points (rollout, eval): grown, never per call
+    size_t io_scratch_bytes = 0;
+    void* io(size_t bytes) {
+        if (io_scratch_bytes < bytes) {
+            if (io_scratch) dfree(io_scratch);
+            io_scratch = dalloc(bytes);
+            io_scratch_bytes = bytes;
+        }
+        return io_scratch;
+    }
 
     bool bf16() const { return cfg.dtype == ALPA_DTYPE_BF16; }
     int64_t ah() const { return cfg.action_hidden_dim; }

@@ -411,3 +411,33 @@ def test_device_open_loop_metrics_on_generated(gen_c1, golden, port):
     ade, div = gen_c1.eval_open_loop(res.trajectories, gt)
     assert ade[0] == port.min_ade(res.trajectories, gt)
     assert div[0] == port.diversity(res.trajectories)
+
+
+# ----------------------------------------------------------------- shape sweep (edge cases)
+@pytest.mark.parametrize("n,r,topology", [
+    (1, 1, "single"), (2, 63, "single"), (3, 64, "multi"), (5, 65, "single"), (7, 127, "multi"),
+    (9, 129, "single"), (13, 300, "multi"), (17, 777, "single"), (20, 2048, "single"),
+])
+def test_persistent_kernel_shape_sweep(port, n, r, topology):
+    """The persistent tensor-core kernel over ragged shapes vs the oracle (bf16
+    bar): prefix lengths around the 64-key block (1, 63-65, 127-129), odd and
+    large lane counts (partial query tiles, several items per CTA), single and
+    multi topology; graph == eager bitwise for each."""
+    m = c2(B=1, K=1)
+    if topology == "single":
+        pre = port.synthetic_prefix(31 + r, 1, r, m.kv_dim)
+        lp = None
+    else:
+        pre = np.stack([port.synthetic_prefix(71 + l, 1, r, m.kv_dim) for l in range(n)])
+        lp = np.arange(n, dtype=np.int32)
+    exp = port.refine(ocfg(m), port.weights(ocfg(m)), pre, port.noise(2, 1, n), lane_prefix=lp)
+    with alpa.ActionGenerator(m) as g:
+        g.bind_prefix(pre)
+        res = g.run_action_generation(alpa.InferenceRequest(num_trajectories=n, topology=topology, v0=5.0))
+        res_e = g.run_action_generation(alpa.InferenceRequest(num_trajectories=n, topology=topology, v0=5.0,
+                                                              executor="eager"))
+    np.testing.assert_array_equal(res.actions, res_e.actions)
+    err = rel_l2(res.actions, exp)
+    print(f"sweep n={n} r={r} {topology}: rel-L2 {err:.3e}")
+    assert err <= BF16_TOL
+    assert res.stats["kernel_launches"] == 1 + 1
