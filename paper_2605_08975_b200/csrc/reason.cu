@@ -383,7 +383,7 @@ void reasoning_prefill(Ctx& c, const float* vision_rows, int64_t P, const int64_
     // the caller's vision rows are [lanes][P][h] (the vision encoder output)
     float* vis = nullptr;
     if (P > 0) {
-        vis = (float*)c.dalloc((size_t)L * P * h * sizeof(float));
+        vis = (float*)c.io((size_t)L * P * h * sizeof(float));  // context scratch, reused
         ALPA_CUDA(cudaMemcpyAsync(vis, vision_rows, (size_t)L * P * h * sizeof(float), cudaMemcpyHostToDevice, s));
     }
     if (n_prompt > 0) {
@@ -407,7 +407,6 @@ void reasoning_prefill(Ctx& c, const float* vision_rows, int64_t P, const int64_
     // the device cache length the captured decode step reads
     ALPA_CUDA(cudaMemcpyAsync(R.dlen, &T, sizeof(int64_t), cudaMemcpyHostToDevice, s));
     ALPA_CUDA(cudaStreamSynchronize(s));
-    if (vis) c.dfree(vis);
     R.T = T;
     R.len = T;
 }
