@@ -16,11 +16,11 @@ pytestmark = pytest.mark.gpu
 R = 256
 
 
-def _cfg():
+def _cfg(dtype="bf16"):
     import paper_2605_08975_b200 as alpa
     return alpa.ModelConfig(vision_blocks=0, hidden_dim=64, vocab_size=128, decoder_blocks=2,
                             action_hidden_dim=256, kv_dim=128, heads=2, diffusion_iters=2,
-                            dtype="bf16")
+                            dtype=dtype)
 
 
 def _free_port():
@@ -31,10 +31,10 @@ def _free_port():
     return p
 
 
-def _direct(scene_seeds, n):
+def _direct(scene_seeds, n, dtype="bf16"):
     import paper_2605_08975_b200 as alpa
     out = []
-    with alpa.ActionGenerator(_cfg()) as g:
+    with alpa.ActionGenerator(_cfg(dtype)) as g:
         for seed in scene_seeds:
             g.bind_prefix_synthetic(seed, R)
             out.append(g.run_action_generation(alpa.InferenceRequest(num_trajectories=n, v0=5.0)))
@@ -148,3 +148,62 @@ def test_two_ranks_share_gpu_batched_scenes(tmp_path):
     mp.spawn(_gloo_two_ranks, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
     ref = np.stack([_split(r) for r in _direct([4242 + 1000 * s for s in range(5)], 4)])
     np.testing.assert_array_equal(np.load(tmp_path / "gloo.npy"), ref)
+
+
+def _gloo_two_ranks_lanes(rank, world, port, out_dir, dtype):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2605_08975_b200 as alpa
+    from paper_2605_08975_b200 import dist as pdist
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g = alpa.ActionGenerator(_cfg(dtype))
+    n_total = 7
+    per = g.prefix_bytes(R)
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    staging = torch.empty(per // staging_esize(dtype), dtype=tdt, device="cuda")
+    prefix = torch.empty(per // staging_esize(dtype), dtype=tdt)  # gloo moves host tensors
+
+    def produce(buf):
+        g.synthesize_prefix(staging.data_ptr(), 4242, R)
+        torch.cuda.synchronize()
+        buf.copy_(staging.cpu())
+
+    def compute(lane0, n_local):
+        staging.copy_(prefix.cuda())
+        torch.cuda.synchronize()
+        g.bind_prefix_device(staging.data_ptr(), 1, R)
+        res = g.run_action_generation(alpa.InferenceRequest(num_trajectories=n_local, lane0=lane0, v0=5.0))
+        return torch.from_numpy(_split(res))
+
+    full = pdist.run_scene(compute, prefix, n_total, root=0, produce=produce)
+    if rank == 0:
+        np.save(os.path.join(out_dir, "lanes.npy"), full.numpy())
+    dist.barrier()
+    g.close()
+    dist.destroy_process_group()
+
+
+def staging_esize(dtype):
+    return 2 if dtype == "bf16" else 4
+
+
+@pytest.mark.parametrize("dtype", ["f32", "bf16"])
+def test_two_ranks_share_gpu_lane_sharded_scene(tmp_path, dtype):
+    """One scene's lanes split over two processes (4 + 3 of 7, global lane
+    seeds): the prefix broadcast from the producing rank, the library on each
+    slice, the gather.  fp32 path: equal to one process computing all 7 lanes
+    bitwise.  bf16 path: the persistent kernel's split-K / KV-split plan
+    depends on the lane count (the reduction order with it), so a slice is
+    equal within the bf16 bar, not bitwise."""
+    import torch.multiprocessing as mp
+
+    mp.spawn(_gloo_two_ranks_lanes, args=(2, _free_port(), str(tmp_path), dtype), nprocs=2, join=True)
+    got = np.load(tmp_path / "lanes.npy")
+    ref = _split(_direct([4242], 7, dtype)[0])
+    if dtype == "f32":
+        np.testing.assert_array_equal(got, ref)
+    else:
+        assert np.linalg.norm(got - ref) / np.linalg.norm(ref) <= 2e-2
