@@ -14,7 +14,9 @@
 // device pointer in the context dtype.
 #pragma once
 
+#include <algorithm>
 #include <array>
+#include <chrono>
 #include <atomic>
 #include <cstdio>
 #include <string>
@@ -111,6 +113,8 @@ struct Trajectory {
 };
 
 // The InferenceRequest fields the path consumes (pipeline.hpp:97-113).
+enum class SampleMode { Greedy, Stochastic };
+
 struct InferenceRequest {
     PoseHistory pose_history;
     std::int64_t num_trajectories = 1;
@@ -119,6 +123,10 @@ struct InferenceRequest {
     ExecMode executor = ExecMode::Eager;
     std::uint64_t action_init_seed = 2;
     std::uint64_t action_seed_stride = 1;
+    // reasoning stage (pipeline.hpp:95-111)
+    std::uint64_t sampler_seed = 1;
+    SampleMode sampler_mode = SampleMode::Stochastic;
+    std::int64_t forced_cot_tokens = 0;
 };
 
 // Sealed reasoning prefix (the part of ReasoningOutput the path reads,
@@ -135,6 +143,12 @@ struct ReasoningOutput {
     std::uint64_t id = next_id();
     std::uint64_t version = 0;
     void touch() { ++version; }
+    // produced by Engine::run_reasoning_device: the KV already sits bound inside
+    // the library (static capacity, in place) -- nothing to upload
+    bool device_resident = false;
+    std::vector<std::vector<std::int64_t>> cot_tokens;  // per lane, no terminator
+    std::int64_t token_count = 0;                       // decode steps executed
+    std::int64_t prompt_tokens = 0;                     // T
 
 private:
     static std::uint64_t next_id() {
@@ -311,10 +325,72 @@ public:
     // LatencyReport (profiler.hpp:31-46, profiler.cpp:31-46 key set) of the last
     // run_action_generation: the action-generation component and its counters;
     // the reasoning / preprocessing components belong to stages outside this path.
+    // Engine::run_reasoning with the language model on the device (SURVEY
+    // §8f-1): vision rows [lanes][P][hidden] (the vision encoder's output, f32)
+    // and the prompt ids in; prefill + the decode loop of reasoning_pass
+    // (pipeline.cpp:279-390) with the reference's sampler; the sealed KV stays
+    // in the library, in place, and the returned ReasoningOutput refers to it.
+    ReasoningOutput run_reasoning_device(const std::vector<float>& vision_rows, std::int64_t patches,
+                                         const std::vector<std::int64_t>& prompt_ids,
+                                         const InferenceRequest& request, std::int64_t max_new_tokens = 256,
+                                         std::int64_t termination_token = 0) {
+        using clk = std::chrono::steady_clock;
+        const std::int64_t lanes = request.topology == Topology::Multi ? request.num_trajectories : 1;
+        if (lanes < 1) throw ConfigError("num_trajectories must be >= 1");
+        const std::int64_t T = patches + static_cast<std::int64_t>(prompt_ids.size());
+        const std::int64_t V = cfg_.vocab_size;
+        const auto t0 = clk::now();
+        check(alpa_reasoning_begin(ctx_, lanes, T + max_new_tokens), ctx_);
+        std::vector<float> logits(static_cast<size_t>(lanes * V));
+        check(alpa_reasoning_prefill(ctx_, vision_rows.data(), patches, prompt_ids.data(),
+                                     static_cast<std::int64_t>(prompt_ids.size()), logits.data()),
+              ctx_);
+        const auto t1 = clk::now();
+        ReasoningOutput out;
+        out.cot_tokens.assign(static_cast<size_t>(lanes), {});
+        out.prompt_tokens = T;
+        std::vector<std::uint64_t> rng(static_cast<size_t>(lanes));
+        for (std::int64_t l = 0; l < lanes; ++l) rng[l] = request.sampler_seed + static_cast<std::uint64_t>(l);
+        std::vector<bool> done(static_cast<size_t>(lanes), false);
+        const bool forced = request.forced_cot_tokens > 0;
+        const std::int64_t max_m = forced ? std::min(request.forced_cot_tokens, max_new_tokens) : max_new_tokens;
+        std::vector<std::int64_t> ids(static_cast<size_t>(lanes));
+        std::int64_t m = 0;
+        while (m < max_m) {
+            bool all_done = true;
+            for (std::int64_t l = 0; l < lanes; ++l) all_done = all_done && done[l];
+            if (all_done && !forced) break;
+            for (std::int64_t l = 0; l < lanes; ++l) {
+                check(alpa_sample_token(logits.data() + l * V, V, request.sampler_mode == SampleMode::Stochastic,
+                                        &rng[l], &ids[l]),
+                      nullptr);
+                if (!done[l]) {
+                    if (!forced && ids[l] == termination_token) done[l] = true;
+                    else out.cot_tokens[l].push_back(ids[l]);
+                }
+            }
+            m += 1;
+            check(alpa_reasoning_decode(ctx_, ids.data(), logits.data()), ctx_);
+        }
+        out.token_count = m;
+        check(alpa_reasoning_seal(ctx_, &out.reasoning_len), ctx_);
+        const auto t2 = clk::now();
+        out.n_prefix = lanes;
+        out.device_resident = true;
+        produced_id_ = out.id;
+        reasoning_prefill_ms_ = std::chrono::duration<double, std::milli>(t1 - t0).count();
+        reasoning_decode_ms_ = std::chrono::duration<double, std::milli>(t2 - t1).count();
+        cot_tokens_ = static_cast<std::int64_t>(out.cot_tokens[0].size());
+        return out;
+    }
+
     LatencyReport latency_report() const {
         LatencyReport r;
+        r.component_ms[2] = reasoning_prefill_ms_;  // LatencyComponent::ReasoningPrefill
+        r.component_ms[3] = reasoning_decode_ms_;   // LatencyComponent::ReasoningDecode
+        r.cot_tokens = cot_tokens_;
         r.component_ms[4] = last_stats_.device_ms;  // LatencyComponent::ActionGen
-        r.total_ms = last_stats_.device_ms;
+        r.total_ms = last_stats_.device_ms + reasoning_prefill_ms_ + reasoning_decode_ms_;
         r.action_gen_iter_ms.assign(last_stats_.iter_ms, last_stats_.iter_ms + last_stats_.n_iter);
         r.alloc_count = 0;  // every buffer is allocated before the first launch
         r.dispatch_count = static_cast<std::uint64_t>(last_stats_.kernel_launches);
@@ -326,6 +402,9 @@ public:
 
 private:
     alpa_stats last_stats_{};
+    std::uint64_t produced_id_ = 0;
+    double reasoning_prefill_ms_ = 0.0, reasoning_decode_ms_ = 0.0;
+    std::int64_t cot_tokens_ = 0;
     static std::vector<float> flatten(const std::vector<Trajectory>& ts) {
         std::vector<float> out;
         for (const Trajectory& t : ts) {
@@ -343,6 +422,11 @@ private:
     // per ReasoningOutput, so a new object at a reused address rebinds), its
     // version (touch()), the data pointers and the shape.
     void bind(const ReasoningOutput& r) {
+        if (r.device_resident) {
+            if (r.id != produced_id_)
+                throw InternalError("device reasoning output of another engine or an earlier scene");
+            return;  // bound by alpa_reasoning_seal
+        }
         const BindKey k{r.id, r.version, r.kv_device, r.kv_host.data(), r.kv_host.size(), r.n_prefix,
                         r.reasoning_len};
         if (bound_valid_ && k == bound_) return;

@@ -6,13 +6,65 @@
 // exit codes follow the reference CLI (cli.cpp:528-540): 1 io, 2 config, 3 internal.
 #include <cstdio>
 #include <fstream>
+#include <string>
 #include <vector>
 
 #include "alpa_minivla_shim.hpp"
 
 using namespace alpa_shim;
 
+// shim_demo --reason <vision.bin f32 [P][hidden]> <P> <prompt.bin int64> <n> <out_actions.bin> <out_traj.bin>:
+// the reasoning stage's language model on the device (Engine::run_reasoning_device),
+// then the action stage on the in-place KV, as Engine::infer sequences them.
+static int reason_mode(char** argv) {
+    ModelConfig cfg;
+    Engine engine(cfg);
+    const std::int64_t P = std::atoll(argv[3]);
+    std::vector<float> vision(static_cast<size_t>(P * cfg.hidden_dim));
+    std::ifstream vin(argv[2], std::ios::binary);
+    if (!vin.read(reinterpret_cast<char*>(vision.data()), vision.size() * sizeof(float)))
+        throw IoError("cannot read vision rows");
+    std::ifstream pin(argv[4], std::ios::binary | std::ios::ate);
+    if (!pin) throw IoError("cannot read prompt ids");
+    std::vector<std::int64_t> prompt(static_cast<size_t>(pin.tellg()) / sizeof(std::int64_t));
+    pin.seekg(0);
+    pin.read(reinterpret_cast<char*>(prompt.data()), prompt.size() * sizeof(std::int64_t));
+    InferenceRequest req;
+    req.num_trajectories = std::atoll(argv[5]);
+    req.topology = Topology::Single;
+    req.kv_strategy = KvStrategy::Static;
+    req.executor = ExecMode::Graph;
+    for (int j = 0; j < 16; ++j) req.pose_history.poses[j] = {-(15.0f - j) * 5.0f * 0.1f, 0.f, 0.f};
+    ReasoningOutput reasoning = engine.run_reasoning_device(vision, P, prompt, req);
+    const auto actions = engine.run_action_generation(reasoning, req);
+    const float v0 = initial_speed_from_history(req.pose_history);
+    std::ofstream oa(argv[6], std::ios::binary), ot(argv[7], std::ios::binary);
+    for (const auto& a : actions) {
+        oa.write(reinterpret_cast<const char*>(a.steps.data()), a.steps.size() * sizeof(ActionStep));
+        const Trajectory t = engine.actions_to_trajectory(a, v0);
+        ot.write(reinterpret_cast<const char*>(t.poses.data()), t.poses.size() * sizeof(Pose));
+    }
+    std::printf("reasoning r=%lld steps=%lld\n", static_cast<long long>(reasoning.reasoning_len),
+                static_cast<long long>(reasoning.token_count));
+    std::printf("report %s\n", engine.latency_report().to_json().c_str());
+    return 0;
+}
+
 int main(int argc, char** argv) {
+    if (argc == 8 && std::string(argv[1]) == "--reason") {
+        try {
+            return reason_mode(argv);
+        } catch (const IoError& e) {
+            std::fprintf(stderr, "io error: %s\n", e.what());
+            return 1;
+        } catch (const ConfigError& e) {
+            std::fprintf(stderr, "config error: %s\n", e.what());
+            return 2;
+        } catch (const InternalError& e) {
+            std::fprintf(stderr, "internal error: %s\n", e.what());
+            return 3;
+        }
+    }
     if (argc != 6) return 1;
     try {
         ModelConfig cfg;  // fixtures/default_config.json model block

@@ -64,3 +64,30 @@ def test_shim_reproduces_golden(tmp_path, golden):
     bad = subprocess.run([exe, str(tmp_path / "nope.bin"), str(r), "6", str(oa), str(ot)],
                          capture_output=True)
     assert bad.returncode == 1
+
+
+@pytest.mark.gpu
+def test_shim_device_reasoning_stage(tmp_path, golden):
+    """Engine::run_reasoning_device (the LM prefill/decode + KV on the device,
+    reference sampler) then the action stage on the in-place KV: the demo
+    scenario's actions / trajectories match the reference's (golden config 1),
+    and the LatencyReport carries the reasoning components and CoT length."""
+    exe = build_demo(tmp_path)
+    rz = np.load(os.path.join(ROOT, "tests", "golden", "reasoning_c1.npz"))
+    vis, prompt = tmp_path / "vision.bin", tmp_path / "prompt.bin"
+    rz["vision"].astype(np.float32).tofile(vis)
+    rz["prompt"].astype(np.int64).tofile(prompt)
+    oa, ot = tmp_path / "a.bin", tmp_path / "t.bin"
+    out = subprocess.run([exe, "--reason", str(vis), str(rz["vision"].shape[0]), str(prompt), "6", str(oa),
+                          str(ot)], capture_output=True, text=True)
+    assert out.returncode == 0, out.stderr
+    acts = np.fromfile(oa, np.float32).reshape(6, 64, 2)
+    traj = np.fromfile(ot, np.float32).reshape(6, 64, 3)
+    ea, et = golden["expected"]["n6_k10_actions"], golden["expected"]["n6_k10_traj"]
+    assert np.linalg.norm(acts - ea) / np.linalg.norm(ea) <= 1e-4
+    assert np.linalg.norm(traj - et) / np.linalg.norm(et) <= 1e-4
+    lines = {ln.split(" ", 1)[0]: ln.split(" ", 1)[1] for ln in out.stdout.splitlines() if " " in ln}
+    assert lines["reasoning"] == f"r={int(rz['r'])} steps={int(rz['m'])}"
+    rep = json.loads(lines["report"])
+    assert rep["reasoning_prefill_ms"] > 0 and rep["reasoning_decode_ms"] > 0
+    assert rep["cot_tokens"] == int(rz["m"]) - 1 and rep["action_gen_ms"] > 0
