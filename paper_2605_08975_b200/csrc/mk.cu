@@ -123,10 +123,13 @@ void mk_prepare(Ctx& c, int64_t n) {
     // >= 64) that still fits one wave -- at N = 6 QKV 24 x 6 = 144 items, O 16 x 6 =
     // 96: their mainloops are bound by the bytes each SM streams, so spreading
     // wins (measured: 64/64 -0.5 ms/scene vs 96/96); the MLPs keep the full tile.
+    // At N = 1 (M = 64) the ops are latency-bound with few items: 32-token tiles
+    // double the SMs streaming QKV / O weights (measured -0.6 ms/scene at N = 1).
+    const int min_tile = M <= 64 ? 32 : 64;
     auto few_tile = [&](int64_t nf) {
         const int64_t tf = nf / 128;
         int best = tn;
-        for (int v = tn; v >= 64; v -= 32)
+        for (int v = tn; v >= min_tile; v -= 32)
             if (tf * ((M + v - 1) / v) <= G) best = v;
         return best;
     };
