@@ -235,6 +235,7 @@ void eval_open_loop_device(Ctx& c, const float* d_traj, const float* d_gt, int64
                            int64_t steps, double* d_min_ade, double* d_div, cudaStream_t s);
 
 // mk.cu: persistent iteration kernel (bf16 path, uniform prefix)
+double gemm_op_cost(int64_t M, int64_t nf, int64_t K, int tn_op, int tn_k, bool split_ok, int G);
 bool mk_usable(const Ctx& c);
 void mk_prepare(Ctx& c, int64_t n);
 void mk_release(Ctx& c);

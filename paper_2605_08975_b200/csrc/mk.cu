@@ -133,7 +133,21 @@ void mk_prepare(Ctx& c, int64_t n) {
             if (tf * ((M + v - 1) / v) <= G) best = v;
         return best;
     };
-    int tno[6] = {few_tile(3 * kv), few_tile(ah), tn, tn, tn, tn};
+    // the deep-K split-K ops (MLP2, encoder MLP2) may take a smaller token tile than
+    // the kernel's when that packs more tiles x splits onto the SMs (cost model)
+    auto split_tile = [&](int64_t nf, int64_t K) {
+        int best = tn;
+        double bt = gemm_op_cost(M, nf, K, tn, tn, true, G);
+        for (int v = tn - 32; v >= 64; v -= 32) {
+            const double t = gemm_op_cost(M, nf, K, v, tn, true, G);
+            if (t < bt * 0.95) {
+                bt = t;
+                best = v;
+            }
+        }
+        return best;
+    };
+    int tno[6] = {few_tile(3 * kv), few_tile(ah), tn, split_tile(ah, 4 * ah), tn, split_tile(ah, 4 * ah)};
     if (const char* e = getenv("ALPA_MK_TN"))
         std::sscanf(e, "%d,%d,%d,%d,%d,%d", &tno[0], &tno[1], &tno[2], &tno[3], &tno[4], &tno[5]);
     for (int& v : tno)

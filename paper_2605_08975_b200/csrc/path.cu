@@ -577,35 +577,59 @@ void launch_attn(Ctx& c, const KInfo& info, int64_t n, int64_t b, cudaStream_t s
 // ingress, ring-latency) per k-block + a per-round drain/sync cost.  Calibrated
 // on B200 measurements over N = 2..64: it picks the measured best
 // tile at 9 of 11 points and is within 5 % at the other two.
+namespace tilemodel {
+int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+int stages(int tn) {
+    int slot = std::max(16384 + tn * 128, 32768);
+    slot = (slot + 1023) / 1024 * 1024;
+    const int aux = std::max(65536, tn * 256 + 12288);
+    return std::min(8, (227 * 1024 - 1024 - aux - 1024) / slot);
+}
+int splits(int64_t tiles, int KB, int tn, int G) {
+    if (tiles >= G) return 1;
+    int best = 1;
+    int64_t used = tiles;
+    for (int s = 2; s <= 4; ++s) {
+        if (tn % s || (tn / s) % 16 || tiles * s > G || KB / s < 2) continue;
+        if ((s - 1) * cdiv(KB, s) >= KB) continue;
+        if (tiles * s > used) {
+            best = s;
+            used = tiles * s;
+        }
+    }
+    while (best > 1) {
+        const int orows = tn / best;
+        if (orows * 768 <= tn * 256 && orows % 16 == 0 && orows <= 64) break;
+        --best;
+        while (best > 1 && tn % best) --best;
+    }
+    return best;
+}
+}  // namespace tilemodel
+
+
+// Modelled time (us) of one GEMM op of the persistent kernel: rounds of items
+// over the SMs (tile quantisation, split-K as the plan picks it) x k-blocks x
+// max(MMA issue max(45, N/2) cycles per 128xNx16 -- tools/mma_rate.cu --,
+// per-SM ingress ~72 B/clk, ring latency ~1 us with the kernel tile's stages in
+// flight) + a per-round drain / sync cost.  Calibrated on B200 sweeps.
+double gemm_op_cost(int64_t M, int64_t nf, int64_t K, int tn_op, int tn_k, bool split_ok, int G) {
+    using namespace tilemodel;
+    const int64_t tiles = (nf / 128) * cdiv(M, tn_op);
+    const int S = split_ok ? splits(tiles, (int)(K / 64), tn_op, G) : 1;
+    const int64_t rounds = cdiv(tiles * S, G);
+    const int64_t kb = cdiv(K / 64, S);
+    const double stage = 16384.0 + tn_op * 128.0;
+    const double mma = 4.0 * std::max(45.0, tn_op / 2.0);
+    const double ingress = stage / 72.0;
+    const double latency = stage / (stages(tn_k) * (16384.0 + tn_k * 128.0)) * 1900.0;
+    return rounds * (kb * std::max(mma, std::max(ingress, latency)) / 1900.0 + (S == 1 ? 3.0 : 6.0));
+}
+
+
 int choose_token_tile(int64_t M, int G) {
     if (M <= 64) return 64;
-    auto cdiv = [](int64_t a, int64_t b) { return (a + b - 1) / b; };
-    auto stages = [](int tn) {
-        int slot = std::max(16384 + tn * 128, 32768);
-        slot = (slot + 1023) / 1024 * 1024;
-        const int aux = std::max(65536, tn * 256 + 12288);
-        return std::min(8, (227 * 1024 - 1024 - aux - 1024) / slot);
-    };
-    auto splits = [&](int64_t tiles, int KB, int tn) {
-        if (tiles >= G) return 1;
-        int best = 1;
-        int64_t used = tiles;
-        for (int s = 2; s <= 4; ++s) {
-            if (tn % s || (tn / s) % 16 || tiles * s > G || KB / s < 2) continue;
-            if ((s - 1) * cdiv(KB, s) >= KB) continue;
-            if (tiles * s > used) {
-                best = s;
-                used = tiles * s;
-            }
-        }
-        while (best > 1) {
-            const int orows = tn / best;
-            if (orows * 768 <= tn * 256 && orows % 16 == 0 && orows <= 64) break;
-            --best;
-            while (best > 1 && tn % best) --best;
-        }
-        return best;
-    };
+    using tilemodel::cdiv;
     auto few = [&](int64_t nf, int tn) {
         int best = tn;
         for (int v = tn; v >= 64; v -= 32)
@@ -613,15 +637,7 @@ int choose_token_tile(int64_t M, int G) {
         return best;
     };
     auto op = [&](int64_t nf, int64_t K, int tn_op, int tn_k, bool split_ok) {
-        const int64_t tiles = (nf / 128) * cdiv(M, tn_op);
-        const int S = split_ok ? splits(tiles, (int)(K / 64), tn_op) : 1;
-        const int64_t rounds = cdiv(tiles * S, G);
-        const int64_t kb = cdiv(K / 64, S);
-        const double stage = 16384.0 + tn_op * 128.0;
-        const double mma = 4.0 * std::max(45.0, tn_op / 2.0);              // cycles per k-block
-        const double ingress = stage / 72.0;                               // ~72 B/clk per SM
-        const double latency = stage / (stages(tn_k) * (16384.0 + tn_k * 128.0)) * 1900.0;  // ~1 us in flight
-        return rounds * (kb * std::max(mma, std::max(ingress, latency)) / 1900.0 + (S == 1 ? 3.0 : 6.0));
+        return gemm_op_cost(M, nf, K, tn_op, tn_k, split_ok, G);
     };
     int best = 192;
     double best_t = 1e30;
