@@ -182,6 +182,32 @@ __device__ inline void tc_mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bde
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// Warp-collective forms: the whole (converged) warp executes them, one elected
+// lane issues.  Keeping the issuing warp's control flow uniform lets ptxas keep
+// the descriptors in uniform registers instead of serialising every operand
+// through R2UR + an ELECT/BRA.U.ANY loop (measured, tools/mma_issue.cu: 56 ->
+// 39 cycles per MMA issue at small N).
+__device__ inline void tc_mma_bf16_w(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc,
+                                     uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p, e;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+__device__ inline void tc_commit_w(uint64_t* bar) {
+    asm volatile(
+        "{\n"
+        ".reg .pred e;\n"
+        "elect.sync _|e, 0xffffffff;\n"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n"
+        "}\n" ::"r"(smem_u32(bar))
+        : "memory");
+}
 // Arrive on an mbarrier once every previously issued tcgen05.mma completed.
 __device__ inline void tc_commit(uint64_t* bar) {
     asm volatile(

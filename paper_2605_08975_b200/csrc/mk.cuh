@@ -137,7 +137,24 @@ enum TraceEv : int {
     TR_LJ = 37,      // attention: K/V block j loads issued (37..41)
     TR_FJ = 42,      // attention: K/V block j landed at the MMA issuer (42..46)
     TR_SX = 48,      // attention softmax of block 1 (thread 0): S ready, S read, exps, P slot free, P stored, arrived (48..53)
-    TR_NSLOT = 64,
+    // SM-clock (clock64) stamps (cycle-precise; the globaltimer ticks at 256 ns here).
+    // Attention item pipeline, MMA thread and softmax thread et 0, block j < 6:
+    TC_MSTART = 64,  // MMA: Q landed
+    TC_MF = 65,      // MMA: K/V block j landed (65..70)
+    TC_MS = 71,      // MMA: S_j issued (71..76)
+    TC_MP = 77,      // MMA: P_j seen (77..82)
+    TC_MPV = 83,     // MMA: PV_j issued (83..88)
+    TC_SS = 89,      // softmax: S_j ready (89..94)
+    TC_SR = 95,      // softmax: S_j in registers (95..100)
+    TC_SE = 101,     // softmax: exps of block j done (101..106)
+    TC_SPF = 107,    // softmax: P slot free (107..112)
+    TC_SA = 113,     // softmax: P_j published (113..118)
+    TC_ACC = 119,    // softmax: all MMAs of the item done
+    TC_MERGE = 120,  // key-half merge + partial stores done
+    // GEMM item, MMA thread: first stage landed, last MMA issued, cycles spent waiting
+    // for landed stages after the first, k-blocks
+    TC_G0 = 64, TC_G1 = 65, TC_GW = 66, TC_GK = 67,
+    TR_NSLOT = 128,
 };
 
 template <int TN, int HD>
@@ -248,6 +265,15 @@ __device__ inline void trace_ev(const Params& p, int o, int ev) {
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
         p.trace[((size_t)o * gridDim.x + blockIdx.x) * TR_NSLOT + ev] = t;
     }
+}
+
+template <bool TR>
+__device__ inline void trace_clk(const Params& p, int o, int ev) {
+    if (TR && p.trace) p.trace[((size_t)o * gridDim.x + blockIdx.x) * TR_NSLOT + ev] = (unsigned long long)clock64();
+}
+template <bool TR>
+__device__ inline void trace_val(const Params& p, int o, int ev, unsigned long long v) {
+    if (TR && p.trace) p.trace[((size_t)o * gridDim.x + blockIdx.x) * TR_NSLOT + ev] = v;
 }
 
 // L2 prefetch of this CTA's 1/G share of a byte range.
@@ -873,7 +899,9 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
         }
     } else if (warp == 1) {
         // ================================================= MMA issuer
-        if (lane == 0) {
+        // the whole warp runs the issue loop (uniform control flow); one elected
+        // lane issues each tcgen05.mma / commit
+        {
             uint32_t ks = 0, nmma = 0, natt = 0, J = 0;
             const uint32_t tS[2] = {tbase, tbase + 64};
             const uint32_t tO[2] = {tbase + 128, tbase + 128 + HD};
@@ -884,21 +912,28 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                     for (int it = blockIdx.x; it < op.n_items; it += gridDim.x) {
                         const GemmItem g = gemm_item(op, it, op.tn);
                         if (nmma > 0) mbar_wait(acc_empty, (nmma - 1) & 1);
+                        unsigned long long wsum = 0;
                         for (int i = 0; i < g.nkb; ++i) {
                             const uint32_t st = (ks + i) % C::STAGES, ph = ((ks + i) / C::STAGES) & 1;
+                            const long long w0 = TR ? clock64() : 0;
                             mbar_wait(&full[st], ph);
-                            if (i == 0) trace_ev<TR>(p, o, TR_MMA0);
+                            if (TR && i > 0) wsum += (unsigned long long)(clock64() - w0);
+                            if (i == 0) if (lane == 0) trace_clk<TR>(p, o, TC_G0);
+                            if (i == 0) if (lane == 0) trace_ev<TR>(p, o, TR_MMA0);
                             tc_fence_after();
                             uint8_t* sb = smem + st * C::SLOT;
                             const uint64_t da = sdesc_k_sw128(sb);
                             const uint64_t db = sdesc_k_sw128(sb + C::W_BYTES);
 #pragma unroll
                             for (int k = 0; k < 4; ++k)
-                                tc_mma_bf16(tbase, da + 2 * k, db + 2 * k, idesc, (i | k) != 0 ? 1u : 0u);
-                            tc_commit(&empty[st]);
+                                tc_mma_bf16_w(tbase, da + 2 * k, db + 2 * k, idesc, (i | k) != 0 ? 1u : 0u);
+                            tc_commit_w(&empty[st]);
                         }
-                        tc_commit(acc_full);
-                        trace_ev<TR>(p, o, TR_MMA1);
+                        tc_commit_w(acc_full);
+                        if (lane == 0) trace_clk<TR>(p, o, TC_G1);
+                        if (lane == 0) trace_val<TR>(p, o, TC_GW, wsum);
+                        if (lane == 0) trace_val<TR>(p, o, TC_GK, (unsigned long long)g.nkb);
+                        if (lane == 0) trace_ev<TR>(p, o, TR_MMA1);
                         ks += g.nkb;
                         ++nmma;
                     }
@@ -922,18 +957,18 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                                     const int ks16 = hh * 2 + kk;  // 16-key step within the block
                                     const uint64_t da = sdesc_k_sw128(pb) + 2 * ks16;
                                     const uint64_t dbv = sdesc_mn_sw128(vb + ks16 * 2048, C::KPANEL);
-                                    tc_mma_bf16(tO[hh], da, dbv, idO, (first && kk == 0) ? 0u : 1u);
+                                    tc_mma_bf16_w(tO[hh], da, dbv, idO, (first && kk == 0) ? 0u : 1u);
                                 }
-                            tc_commit(&empty[st]);
-                            tc_commit(&p_free[JJ & 1]);
+                            tc_commit_w(&empty[st]);
+                            tc_commit_w(&p_free[JJ & 1]);
                         };
                         uint32_t prev_st = 0;
                         for (int j = 0; j < a.nj; ++j) {
                             const uint32_t JJ = J + j;
                             const uint32_t st = (ks + j) % C::STAGES, ph = ((ks + j) / C::STAGES) & 1;
                             mbar_wait(&full[st], ph);
-                            if (j == 0) trace_ev<TR>(p, o, TR_MMA0);
-                            if (j < 5) trace_ev<TR>(p, o, TR_FJ + j);
+                            if (j == 0) if (lane == 0) trace_ev<TR>(p, o, TR_MMA0);
+                            if (j < 5) if (lane == 0) trace_ev<TR>(p, o, TR_FJ + j);
                             if (JJ >= 2) mbar_wait(&s_free[JJ & 1], ((JJ - 2) >> 1) & 1);
                             tc_fence_after();
                             const uint8_t* kb = smem + st * C::SLOT;
@@ -941,18 +976,18 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                             for (int kk = 0; kk < HD / 16; ++kk) {
                                 const uint64_t da = sdesc_k_sw128(smem + C::OFF_Q + (kk >> 2) * C::QPANEL) + 2 * (kk & 3);
                                 const uint64_t db = sdesc_k_sw128(kb + (kk >> 2) * C::KPANEL) + 2 * (kk & 3);
-                                tc_mma_bf16(tS[JJ & 1], da, db, idS, kk > 0 ? 1u : 0u);
+                                tc_mma_bf16_w(tS[JJ & 1], da, db, idS, kk > 0 ? 1u : 0u);
                             }
-                            tc_commit(&s_full[JJ & 1]);
-                            if (j < 5) trace_ev<TR>(p, o, TR_SJ + j);
-                            if (j == a.nj - 1) tc_commit(q_empty);
+                            tc_commit_w(&s_full[JJ & 1]);
+                            if (j < 5) if (lane == 0) trace_ev<TR>(p, o, TR_SJ + j);
+                            if (j == a.nj - 1) tc_commit_w(q_empty);
                             if (j > 0) issue_pv(JJ - 1, prev_st, j == 1);
                             prev_st = st;
                         }
                         if (a.nj > 0) issue_pv(J + a.nj - 1, prev_st, a.nj == 1);
-                        else tc_commit(q_empty);
-                        tc_commit(acc_full);
-                        trace_ev<TR>(p, o, TR_MMA1);
+                        else tc_commit_w(q_empty);
+                        tc_commit_w(acc_full);
+                        if (lane == 0) trace_ev<TR>(p, o, TR_MMA1);
                         ks += a.nj;
                         J += a.nj;
                         ++natt;

@@ -3,7 +3,7 @@
 #include <cstdio>
 #include <cuda_runtime.h>
 
-__global__ void __launch_bounds__(320, 1) k(int* out) {
+__global__ void __launch_bounds__(384, 1) k(int* out) {
     extern __shared__ unsigned char sm[];
     sm[threadIdx.x] = 1;
     unsigned r;
@@ -20,7 +20,7 @@ int main() {
     for (int cs : {1, 2, 3, 4, 6, 8, 16}) {
         cudaLaunchConfig_t cfg{};
         cfg.gridDim = dim3(cs * 16);
-        cfg.blockDim = dim3(320);
+        cfg.blockDim = dim3(384);
         cfg.dynamicSmemBytes = smem;
         cudaLaunchAttribute at[2];
         at[0].id = cudaLaunchAttributeClusterDimension;

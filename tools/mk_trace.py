@@ -41,7 +41,7 @@ nops, grid = C.c_int64(), C.c_int64()
 rc = L.alpa_debug_mk_trace(g._h, buf.ctypes.data_as(C.POINTER(C.c_ulonglong)), buf.size,
                            C.byref(nops), C.byref(grid))
 assert rc == 0, rc
-NS = 64  # mk::TR_NSLOT
+NS = 128  # mk::TR_NSLOT
 tr = buf[: nops.value * grid.value * NS].reshape(nops.value, grid.value, NS).astype(np.int64)
 if a.dump:
     np.savez_compressed(a.dump, trace=tr)
