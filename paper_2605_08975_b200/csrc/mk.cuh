@@ -944,9 +944,11 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                         const AttnItem a = attn_item(op, it, p.M);
                         if (nmma > 0) mbar_wait(acc_empty, (nmma - 1) & 1);
                         mbar_wait(q_full, natt & 1);
+                        if (lane == 0) trace_clk<TR>(p, o, TC_MSTART);
                         tc_fence_after();
                         auto issue_pv = [&](uint32_t JJ, uint32_t st, bool first) {
                             mbar_wait(&p_full[JJ & 1], (JJ >> 1) & 1);
+                            if (JJ - J < 6) if (lane == 0) trace_clk<TR>(p, o, TC_MP + (JJ - J));
                             tc_fence_after();
                             const uint8_t* pb = smem + C::OFF_P + (JJ & 1) * C::P_BYTES;
                             const uint8_t* vb = smem + st * C::SLOT + C::KVB;
@@ -961,6 +963,7 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                                 }
                             tc_commit_w(&empty[st]);
                             tc_commit_w(&p_free[JJ & 1]);
+                            if (JJ - J < 6) if (lane == 0) trace_clk<TR>(p, o, TC_MPV + (JJ - J));
                         };
                         uint32_t prev_st = 0;
                         for (int j = 0; j < a.nj; ++j) {
@@ -969,6 +972,7 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                             mbar_wait(&full[st], ph);
                             if (j == 0) if (lane == 0) trace_ev<TR>(p, o, TR_MMA0);
                             if (j < 5) if (lane == 0) trace_ev<TR>(p, o, TR_FJ + j);
+                            if (j < 6) if (lane == 0) trace_clk<TR>(p, o, TC_MF + j);
                             if (JJ >= 2) mbar_wait(&s_free[JJ & 1], ((JJ - 2) >> 1) & 1);
                             tc_fence_after();
                             const uint8_t* kb = smem + st * C::SLOT;
@@ -979,6 +983,7 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                                 tc_mma_bf16_w(tS[JJ & 1], da, db, idS, kk > 0 ? 1u : 0u);
                             }
                             tc_commit_w(&s_full[JJ & 1]);
+                            if (j < 6) if (lane == 0) trace_clk<TR>(p, o, TC_MS + j);
                             if (j < 5) if (lane == 0) trace_ev<TR>(p, o, TR_SJ + j);
                             if (j == a.nj - 1) tc_commit_w(q_empty);
                             if (j > 0) issue_pv(JJ - 1, prev_st, j == 1);
@@ -1328,6 +1333,7 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                         const uint32_t JJ = J + j, b = JJ & 1;
                         mbar_wait(&s_full[b], (JJ >> 1) & 1);
                         if (j == 0 && et == 0) trace_ev<TR>(p, o, TR_SM0);
+                        if (j < 6 && et == 0) trace_clk<TR>(p, o, TC_SS + j);
                         const bool trj = TR && j == 1 && et == 0;
                         if (trj) trace_ev<TR>(p, o, TR_SX + 0);
                         tc_fence_after();
@@ -1338,6 +1344,7 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&s_free[b]);
                         if (trj) trace_ev<TR>(p, o, TR_SX + 1);
+                        if (j < 6 && et == 0) trace_clk<TR>(p, o, TC_SR + j);
                         const int gb = a.g0 + j;
                         // keys of this (row, half) in the block: warp-uniform (a warp's 32 rows
                         // belong to one lane: i >> 6 = q >> 1); all 32 except the prefix tail
@@ -1393,8 +1400,10 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                         }
                         l = l * corr + rsum;
                         if (trj) trace_ev<TR>(p, o, TR_SX + 2);
+                        if (j < 6 && et == 0) trace_clk<TR>(p, o, TC_SE + j);
                         if (JJ >= 2) mbar_wait(&p_free[b], ((JJ - 2) >> 1) & 1);
                         if (trj) trace_ev<TR>(p, o, TR_SX + 3);
+                        if (j < 6 && et == 0) trace_clk<TR>(p, o, TC_SPF + j);
                         uint8_t* prow = smem + C::OFF_P + b * C::P_BYTES + i * 128;
 #pragma unroll
                         for (int c = 0; c < 4; ++c) {
@@ -1423,6 +1432,7 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                         __syncwarp();
                         if (lane == 0) mbar_arrive(&p_full[b]);
                         if (trj) trace_ev<TR>(p, o, TR_SX + 5);
+                        if (j < 6 && et == 0) trace_clk<TR>(p, o, TC_SA + j);
                         if (et == 0 && j < 5) trace_ev<TR>(p, o, TR_SMJ + j);
                     }
                     J += a.nj;
@@ -1433,6 +1443,7 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                     // (scratch overlaps the P tiles: only after the last PV completed)
                     mbar_wait(acc_full, nmma & 1);
                     if (et == 0) trace_ev<TR>(p, o, TR_ACC);
+                    if (et == 0) trace_clk<TR>(p, o, TC_ACC);
                     tc_fence_after();
                     float* mlx = reinterpret_cast<float*>(smem + C::OFF_SCR);  // [2][2][128]
                     mlx[(hh * 2 + 0) * 128 + i] = m_ref;
@@ -1496,6 +1507,7 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                         fence_proxy_async_global();
                     }
                     if (et == 0) trace_ev<TR>(p, o, TR_MERGE);
+                    if (et == 0) trace_clk<TR>(p, o, TC_MERGE);
                     tc_fence_before();
                     epi_bar();
                     if (et == 0) mbar_arrive(acc_empty);

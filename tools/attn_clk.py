@@ -16,9 +16,9 @@ def med(i):
     return np.median(v[ok] - r[ok, 64]) if ok.any() else float("nan")
 
 
-names = [("S deps", 123), ("S issued", 71), ("PV issued", 83), ("S ready", 89), ("S read", 95), ("exps", 101), ("P slot", 107),
+names = [("K/V seen", 65), ("S issued", 71), ("PV issued", 83), ("S ready", 89), ("S read", 95), ("exps", 101), ("P slot", 107),
          ("P pub", 113)]
 print("block " + "".join(f"{n:>11s}" for n, _ in names))
 for j in range(6):
-    print(f"{j:5d} " + "".join(f"{med(i + j) if i != 123 or j < 5 else float('nan'):11.0f}" for _, i in names))
+    print(f"{j:5d} " + "".join(f"{med(i + j)   :11.0f}" for _, i in names))
 print(f"all MMAs done {med(119):.0f}  merge+partials stored {med(120):.0f}  (cycles)")
