@@ -445,6 +445,7 @@ struct DrainArgs {
     const CUtensorMap* te16; // fp32 box {32, 16, 1} or null
     int f0, t0, hh;
     float2* st_part;         // row-stat partials [4][256] or null
+    unsigned long long* clk; // diagnostics (traced twin, et 0): clock64 per chunk phase, or null
 };
 template <bool LN, bool GELU, bool RESID, bool F32, bool STATS>
 __device__ __forceinline__ void drain_t(const DrainArgs& a) {
@@ -463,6 +464,7 @@ __device__ __forceinline__ void drain_t(const DrainArgs& a) {
             tmem_ld16x256b_x2(a.tres + (16u << 16) + c, RB);
         }
         tmem_ld_wait();
+        if (a.clk && c < 64) a.clk[(c >> 4) * 4 + 0] = clock64();
         // v[k][m]: feature fa + 8k, token t_m = cb + c + (m >> 1) * 8 + 2 tq + (m & 1)
         float v[4][4];
 #pragma unroll
@@ -530,11 +532,13 @@ __device__ __forceinline__ void drain_t(const DrainArgs& a) {
                                   pack_bf16x2(v[2][2 * g], v[2][2 * g + 1]), pack_bf16x2(v[3][2 * g], v[3][2 * g + 1]));
             }
         }
+        if (a.clk && c < 64) a.clk[(c >> 4) * 4 + 1] = clock64();
         if (a.tm16) {
             // this chunk's 16 rows of the half are staged by its 4 warps: store them now
             // (the store overlaps the rest of the drain instead of trailing it)
             fence_proxy_async();
             asm volatile("bar.sync %0, 128;" ::"r"(3 + a.hh) : "memory");
+            if (a.clk && c < 64) a.clk[(c >> 4) * 4 + 2] = clock64();
             if (a.q == 0 && a.lane == 0) {
                 const int r = a.cb + c;
                 tma_store_2d(a.tm16, a.stg + r * 128, a.f0, a.t0 + r);
@@ -546,6 +550,7 @@ __device__ __forceinline__ void drain_t(const DrainArgs& a) {
                 }
                 bulk_commit();
             }
+            if (a.clk && c < 64) a.clk[(c >> 4) * 4 + 3] = clock64();
         }
         if constexpr (STATS) {
             // per token: sum over the thread's 4 features, then over the 8 lanes
@@ -1184,6 +1189,7 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                     }
                     mbar_wait(acc_full, nmma & 1);
                     if (et == 0) trace_ev<TR>(p, o, TR_ACC);
+                    if (et == 0) trace_clk<TR>(p, o, 68);
                     tc_fence_after();
                     {
                         if (!split_path) {
@@ -1209,6 +1215,9 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                             da.estg = (f32o && op.tmEs) ? stg_base + TNo * 256 : nullptr;
                             da.tn = TNo;
                             da.st_part = st_part;
+                            da.clk = (TR && p.trace && et == 0)
+                                         ? p.trace + ((size_t)o * gridDim.x + blockIdx.x) * TR_NSLOT + 72
+                                         : nullptr;
                             da.tm16 = op.tmO16;
                             da.te16 = (f32o && op.tmEs) ? op.tmE16 : nullptr;
                             da.f0 = g.f0;
@@ -1237,6 +1246,7 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                         }
                     }
                     if (et == 0) trace_ev<TR>(p, o, TR_LOOP);
+                    if (et == 0) trace_clk<TR>(p, o, 69);
                     if (!split_path && !op.tmO16) {
                         // staged bf16 tile (output, or the residual's bf16 copy) -> TMA store
                         fence_proxy_async();
