@@ -779,7 +779,9 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(C::REG_LO));
     if (warp == 0) {
         // ================================================= TMA producer
-        if (lane == 0) {
+        // the whole warp runs the producer loop (uniform control flow); one elected
+        // lane issues each TMA load / expect_tx
+        {
             uint32_t ks = 0, natt = 0;
             // weights and the prefix are streamed once per iteration: evict_first
             // keeps them from displacing the kernel's code and the activations in L2
@@ -793,8 +795,8 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
             for (int o = 0; o < p.n_ops; ++o) {
                 const Op op = p.ops[o];  // register copy: stores must not force reloads
                 if (op.kind == OP_GEMM) {
-                    tma_prefetch(op.tmW);
-                    tma_prefetch(op.tmX);
+                    if (lane == 0) tma_prefetch(op.tmW);
+                    if (lane == 0) tma_prefetch(op.tmX);
                     bool waited = false;
                     for (int it = blockIdx.x; it < op.n_items; it += gridDim.x) {
                         const GemmItem g = gemm_item(op, it, op.tn);
@@ -812,33 +814,33 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                         for (int i = 0; i < pre; ++i) {
                             const uint32_t st = (ks + i) % C::STAGES;
                             uint8_t* sb = slot_acquire(ks + i);
-                            mbar_expect_tx(&full[st], stage_tx);
-                            tma_load_2d_hint(sb, op.tmW, &full[st], (g.kb0 + i) * 64, g.f0, wpol);
+                            mbar_expect_tx_w(&full[st], stage_tx);
+                            tma_load_2d_hint_w(sb, op.tmW, &full[st], (g.kb0 + i) * 64, g.f0, wpol);
                         }
-                        trace_ev<TR>(p, o, TR_PRE);
+                        if (lane == 0) trace_ev<TR>(p, o, TR_PRE);
                         if (!waited && op.dep >= 0) {
                             wait_count<TR>(p.done + op.dep, op.dep_count);
                             fence_proxy_async_global();
                             waited = true;
                         }
-                        trace_ev<TR>(p, o, TR_DEP);
+                        if (lane == 0) trace_ev<TR>(p, o, TR_DEP);
                         for (int i = 0; i < g.nkb; ++i) {
                             const uint32_t st = (ks + i) % C::STAGES;
                             uint8_t* sb = smem + st * C::SLOT;
                             if (i >= pre) {
                                 sb = slot_acquire(ks + i);
-                                mbar_expect_tx(&full[st], stage_tx);
-                                tma_load_2d_hint(sb, op.tmW, &full[st], (g.kb0 + i) * 64, g.f0, wpol);
+                                mbar_expect_tx_w(&full[st], stage_tx);
+                                tma_load_2d_hint_w(sb, op.tmW, &full[st], (g.kb0 + i) * 64, g.f0, wpol);
                             }
-                            tma_load_2d(sb + C::W_BYTES, op.tmX, &full[st], (g.kb0 + i) * 64, g.t0);
+                            tma_load_2d_w(sb + C::W_BYTES, op.tmX, &full[st], (g.kb0 + i) * 64, g.t0);
                         }
                         ks += g.nkb;
                     }
-                    if (!(p.flags & MK_NO_L2PF)) l2_share(op.pf_ptr, op.pf_bytes, wpol);
+                    if (lane == 0 && !(p.flags & MK_NO_L2PF)) l2_share(op.pf_ptr, op.pf_bytes, wpol);
                 } else if (op.kind == OP_ATTN) {
-                    tma_prefetch(op.tmW);
-                    tma_prefetch(op.tmX);
-                    tma_prefetch(op.tmQ);
+                    if (lane == 0) tma_prefetch(op.tmW);
+                    if (lane == 0) tma_prefetch(op.tmX);
+                    if (lane == 0) tma_prefetch(op.tmQ);
                     bool waited = false;
                     for (int it = blockIdx.x; it < op.n_items; it += gridDim.x) {
                         const AttnItem a = attn_item(op, it, p.M);
@@ -851,21 +853,21 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                         auto load_block = [&](int j) {
                             const uint32_t st = (ks + j) % C::STAGES;
                             uint8_t* kb = slot_acquire(ks + j);
-                            if (j < 5) trace_ev<TR>(p, o, TR_LJ + j);
+                            if (j < 5) if (lane == 0) trace_ev<TR>(p, o, TR_LJ + j);
                             uint8_t* vb = kb + C::KVB;
-                            mbar_expect_tx(&full[st], 2 * C::KVB);
+                            mbar_expect_tx_w(&full[st], 2 * C::KVB);
                             const int gb = a.g0 + j;
                             for (int pn = 0; pn < HD / 64; ++pn) {
                                 const int col = a.h * HD + pn * 64;
                                 if (gb < op.nbp) {
-                                    tma_load_2d_hint(kb + pn * C::KPANEL, op.tmW, &full[st], col,
+                                    tma_load_2d_hint_w(kb + pn * C::KPANEL, op.tmW, &full[st], col,
                                                      (int)(pre_k + gb * 64), ppol);
-                                    tma_load_2d_hint(vb + pn * C::KPANEL, op.tmW, &full[st], col,
+                                    tma_load_2d_hint_w(vb + pn * C::KPANEL, op.tmW, &full[st], col,
                                                      (int)(pre_v + gb * 64), ppol);
                                 } else {
                                     const int row = a.row0 + (gb - op.nbp) * 64;
-                                    tma_load_2d(kb + pn * C::KPANEL, op.tmX, &full[st], p.kv + col, row);
-                                    tma_load_2d(vb + pn * C::KPANEL, op.tmX, &full[st], 2 * p.kv + col, row);
+                                    tma_load_2d_w(kb + pn * C::KPANEL, op.tmX, &full[st], p.kv + col, row);
+                                    tma_load_2d_w(vb + pn * C::KPANEL, op.tmX, &full[st], 2 * p.kv + col, row);
                                 }
                             }
                         };
@@ -878,27 +880,27 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                             for (int j = pre; j < a.nj && a.g0 + j < op.nbp; ++j)
 #pragma unroll 1
                                 for (int pn = 0; pn < HD / 64; ++pn) {
-                                    tma_prefetch_box_2d(op.tmW, a.h * HD + pn * 64, (int)(pre_k + (a.g0 + j) * 64));
-                                    tma_prefetch_box_2d(op.tmW, a.h * HD + pn * 64, (int)(pre_v + (a.g0 + j) * 64));
+                                    if (lane == 0) tma_prefetch_box_2d(op.tmW, a.h * HD + pn * 64, (int)(pre_k + (a.g0 + j) * 64));
+                                    if (lane == 0) tma_prefetch_box_2d(op.tmW, a.h * HD + pn * 64, (int)(pre_v + (a.g0 + j) * 64));
                                 }
                         }
-                        trace_ev<TR>(p, o, TR_PRE);
+                        if (lane == 0) trace_ev<TR>(p, o, TR_PRE);
                         if (!waited && op.dep >= 0) {
                             wait_count<TR>(p.done + op.dep, op.dep_count);
                             fence_proxy_async_global();
                             waited = true;
                         }
-                        trace_ev<TR>(p, o, TR_DEP);
+                        if (lane == 0) trace_ev<TR>(p, o, TR_DEP);
                         if (natt > 0) mbar_wait(q_empty, (natt - 1) & 1);
-                        mbar_expect_tx(q_full, C::Q_BYTES);
+                        mbar_expect_tx_w(q_full, C::Q_BYTES);
                         for (int pn = 0; pn < HD / 64; ++pn)
-                            tma_load_2d(smem + C::OFF_Q + pn * C::QPANEL, op.tmQ, q_full,
+                            tma_load_2d_w(smem + C::OFF_Q + pn * C::QPANEL, op.tmQ, q_full,
                                         a.h * HD + pn * 64, a.row0);
                         for (int j = pre; j < a.nj; ++j) load_block(j);
                         ks += a.nj;
                         ++natt;
                     }
-                    if (!(p.flags & MK_NO_L2PF)) l2_share(op.pf_ptr, op.pf_bytes, wpol);
+                    if (lane == 0 && !(p.flags & MK_NO_L2PF)) l2_share(op.pf_ptr, op.pf_bytes, wpol);
                 }
             }
         }
