@@ -249,6 +249,8 @@ void make_tmap_bf16_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_
                        uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer);
 void make_tmap_f32_2d(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
                       uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer);
+void make_tmap_panels(CUtensorMap* m, const void* base, bool f32, uint64_t cols, uint64_t rows,
+                      uint64_t row_stride_bytes, uint32_t box_rows, uint32_t panels);
 void make_tmap_f32_3d_sw128(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2,
                             uint64_t stride1_bytes, uint64_t stride2_bytes, uint32_t box1);
 

@@ -234,8 +234,15 @@ void mk_prepare(Ctx& c, int64_t n) {
         op.tmXB = produce ? dm(act_map(c.ws.x, ah, ttn)) : nullptr;
         // progressive 16-row stores of the unsplit drain (ALPA_MK_PROG=0: one store per tile)
         const bool prog = !getenv("ALPA_MK_PROG") || getenv("ALPA_MK_PROG")[0] != '0';
-        if (prog && (op.tmO || op.tmXB))
-            op.tmO16 = dm(op.tmO ? act_map(out, L.out, 16) : act_map(c.ws.x, ah, 16));
+        if (prog && (op.tmO || op.tmXB)) {
+            // one store per 16-row chunk across both 64-feature panels (chunk-major staging)
+            CUtensorMap tp{};
+            if (op.tmO)
+                make_tmap_panels(&tp, out, false, (uint64_t)L.out, (uint64_t)M, (uint64_t)L.out * 2, 16, 2);
+            else
+                make_tmap_panels(&tp, c.ws.x, false, (uint64_t)ah, (uint64_t)M, (uint64_t)ah * 2, 16, 2);
+            op.tmO16 = dm(add_map(tp));
+        }
         if (op.splits == 1 && (epi == EPI_RESID_F32 || epi == EPI_F32) && (size_t)ttn * (256 + 512) <= (size_t)tn * 256) {
             // unsplit fp32 producer whose fp32 tile fits the staging next to the bf16 tile:
             // TMA-stored through four SW128 panels of 32 fp32 (box {32, TN, 1})
@@ -243,8 +250,8 @@ void mk_prepare(Ctx& c, int64_t n) {
             make_tmap_f32_3d_sw128(&te, out, (uint64_t)L.out, (uint64_t)M, 1, (uint64_t)ldo * 4,
                                    (uint64_t)ldo * 4 * M, (uint32_t)ttn);
             op.tmEs = dm(add_map(te));
-            make_tmap_f32_3d_sw128(&te, out, (uint64_t)L.out, (uint64_t)M, 1, (uint64_t)ldo * 4,
-                                   (uint64_t)ldo * 4 * M, 16);
+            // progressive: one store per 16-row chunk across the four 32-fp32 panels
+            make_tmap_panels(&te, out, true, (uint64_t)L.out, (uint64_t)M, (uint64_t)ldo * 4, 16, 4);
             op.tmE16 = dm(add_map(te));
         }
         if (op.splits > 1) {

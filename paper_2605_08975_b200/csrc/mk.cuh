@@ -62,8 +62,8 @@ struct Op {
     const CUtensorMap* tmXB; // GEMM, unsplit residual producer: bf16 copy map, box {64,TN}
     const CUtensorMap* tmEs; // GEMM fp32 producer: split -> fp32 rows, box {128, TN/S}; unsplit -> SW128 box {32, TN, 1}
     const CUtensorMap* tmXs; // GEMM, split residual producer: bf16 copy, box {64, TN/S}
-    const CUtensorMap* tmO16; // GEMM, unsplit: bf16 output (or the residual's bf16 copy), box {64, 16}
-    const CUtensorMap* tmE16; // GEMM, unsplit fp32 staging: SW128 box {32, 16, 1}
+    const CUtensorMap* tmO16; // GEMM, unsplit: bf16 output (or the residual's bf16 copy), 16-row chunk x 2 panels
+    const CUtensorMap* tmE16; // GEMM, unsplit fp32 output: 16-row chunk x 4 SW128 panels (chunk-major staging)
                              // attention: fp32 KV-split partials [S][M][kv], box {32, 128, 1} SW128
     const float* bias;
     const float* colsum;     // LN-folded consumers
@@ -453,7 +453,11 @@ __device__ __forceinline__ void drain_t(const DrainArgs& a) {
     // stmatrix row addresses: matrix i = lane >> 3 (features 8i..), row j = lane & 7 (token)
     const int mj = a.lane & 7;
     const int chunk = (a.q & 1) * 4 + (a.lane >> 3);
-    const uint32_t sbase = a.stg ? smem_u32(a.stg) + (a.q >> 1) * (a.tn * 128) : 0u;
+    // staging layout: progressive stores (tm16) keep each 16-row chunk's panels together
+    // ([chunk][panel][16 rows][128 B], one 3-D TMA store per chunk); whole-tile stores
+    // use [panel][TN rows][128 B]
+    const bool cm = a.tm16 != nullptr;
+    const uint32_t sbase = a.stg ? smem_u32(a.stg) + (a.q >> 1) * (cm ? 2048 : a.tn * 128) : 0u;
 #pragma unroll 1
     for (int c = 0; c < a.ncol; c += 16) {
         uint32_t A[8], B[8], RA[8], RB[8];
@@ -507,8 +511,10 @@ __device__ __forceinline__ void drain_t(const DrainArgs& a) {
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
                         const int fq = a.q * 32 + tr + 8 * k;  // feature within the tile
-                        *reinterpret_cast<float*>(a.estg + (fq >> 5) * (a.tn * 128) + r * 128 +
-                                                  (((((fq & 31) >> 2) ^ (r & 7))) << 4) + (fq & 3) * 4) = v[k][m];
+                        const int off = cm ? (r >> 4) * 8192 + (fq >> 5) * 2048 + (r & 15) * 128
+                                           : (fq >> 5) * (a.tn * 128) + r * 128;
+                        *reinterpret_cast<float*>(a.estg + off + (((((fq & 31) >> 2) ^ (r & 7))) << 4) + (fq & 3) * 4) =
+                            v[k][m];
                     }
                 }
             } else {
@@ -527,7 +533,7 @@ __device__ __forceinline__ void drain_t(const DrainArgs& a) {
 #pragma unroll
             for (int g = 0; g < 2; ++g) {
                 const int tok = a.cb + c + g * 8 + mj;
-                stmatrix_x4_trans(sbase + tok * 128 + ((chunk ^ (tok & 7)) << 4),
+                stmatrix_x4_trans(sbase + (cm ? (tok >> 4) * 4096 + (tok & 15) * 128 : tok * 128) + ((chunk ^ (tok & 7)) << 4),
                                   pack_bf16x2(v[0][2 * g], v[0][2 * g + 1]), pack_bf16x2(v[1][2 * g], v[1][2 * g + 1]),
                                   pack_bf16x2(v[2][2 * g], v[2][2 * g + 1]), pack_bf16x2(v[3][2 * g], v[3][2 * g + 1]));
             }
@@ -541,13 +547,8 @@ __device__ __forceinline__ void drain_t(const DrainArgs& a) {
             if (a.clk && c < 64) a.clk[(c >> 4) * 4 + 2] = clock64();
             if (a.q == 0 && a.lane == 0) {
                 const int r = a.cb + c;
-                tma_store_2d(a.tm16, a.stg + r * 128, a.f0, a.t0 + r);
-                tma_store_2d(a.tm16, a.stg + a.tn * 128 + r * 128, a.f0 + 64, a.t0 + r);
-                if (a.te16) {
-#pragma unroll
-                    for (int pn = 0; pn < 4; ++pn)
-                        tma_store_3d(a.te16, a.estg + pn * (a.tn * 128) + r * 128, a.f0 + 32 * pn, a.t0 + r, 0);
-                }
+                tma_store_3d(a.tm16, a.stg + (r >> 4) * 4096, 0, a.t0 + r, a.f0 >> 6);
+                if (a.te16) tma_store_3d(a.te16, a.estg + (r >> 4) * 8192, 0, a.t0 + r, a.f0 >> 5);
                 bulk_commit();
             }
             if (a.clk && c < 64) a.clk[(c >> 4) * 4 + 3] = clock64();

@@ -69,4 +69,23 @@ void make_tmap_f32_3d_sw128(CUtensorMap* m, const void* base, uint64_t d0, uint6
         fail(ALPA_ERR_INTERNAL, "cuTensorMapEncodeTiled (f32 3d) failed (" + std::to_string((int)r) + ")");
 }
 
+// 3-D "panel" view of a row-major [rows][cols] tensor for one-instruction stores of
+// a 16-row chunk across several 128-byte panels: dims {panel elems, rows, cols /
+// panel elems}, strides {row bytes, 128 B}, box {panel elems, box_rows, panels},
+// SWIZZLE_128B.  The smem box is [panels][box_rows][128 B] (chunk-major staging).
+void make_tmap_panels(CUtensorMap* m, const void* base, bool f32, uint64_t cols, uint64_t rows,
+                      uint64_t row_stride_bytes, uint32_t box_rows, uint32_t panels) {
+    const uint64_t pe = f32 ? 32 : 64;  // elements per 128-byte panel row
+    cuuint64_t dims[3] = {pe, rows, cols / pe};
+    cuuint64_t strides[2] = {row_stride_bytes, 128};
+    cuuint32_t box[3] = {(cuuint32_t)pe, box_rows, panels};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = encode_fn()(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3,
+                             const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS)
+        fail(ALPA_ERR_INTERNAL, "cuTensorMapEncodeTiled (panels) failed (" + std::to_string((int)r) + ")");
+}
+
 }  // namespace alpa
