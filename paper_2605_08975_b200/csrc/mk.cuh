@@ -702,6 +702,7 @@ __device__ inline void publish(const Params& p, int o, int et) {
     if (et == 0) {
         trace_ev<TR>(p, o, TR_FENCE);
         red_release_add(p.done + o, 1);  // release is cumulative over the CTA's writes (bar.sync)
+        trace_clk<TR>(p, o, 95);
         stamp<TR>(p, o);
         trace_ev<TR>(p, o, TR_PUB);
     }
@@ -1273,7 +1274,9 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                     if (et == 0) mbar_arrive(acc_empty);
                     ++nmma;
                     if (split_path) {
+                        if (et == 0) trace_clk<TR>(p, o, 90);
                         split_meet<TR>(p, op, o, p.splitc + op.split_base + g.tile, et);
+                        if (et == 0) trace_clk<TR>(p, o, 91);
                         // finalise the owned tokens in the TMEM layout: own partial from
                         // TMEM + the other splits' partials + bias (+ staged residual) ->
                         // fp32 staging; then the row pass (stats + bf16 copy) and TMA stores
@@ -1298,6 +1301,7 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                                     : nullptr;
                         if (resid) fix_t<true, TR>(fa);
                         else fix_t<false, TR>(fa);
+                        if (et == 0) trace_clk<TR>(p, o, 92);
                         if (et == 0) trace_ev<TR>(p, o, TR_FIXED);
                         // the fp32 rows leave while the row pass builds the stats and bf16 copy
                         fence_proxy_async();
@@ -1307,6 +1311,7 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                             tma_store_2d(op.tmEs, smem + C::OFF_STG, g.f0, g.t0 + own_lo);
                             bulk_commit();
                         }
+                        if (et == 0) trace_clk<TR>(p, o, 93);
                         fix_rows(e_stg, x_stg, orows, n_own,
                                  op.stats_out ? op.stats_out + (int64_t)(g.t0 + own_lo) * p.nft + g.f0 / 128 : nullptr,
                                  p.nft, et);
@@ -1317,6 +1322,7 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                             tma_store_2d(op.tmXs, x_stg + orows * 128, g.f0 + 64, g.t0 + own_lo);
                             bulk_commit();
                         }
+                        if (et == 0) trace_clk<TR>(p, o, 94);
                         if (et == 0) trace_ev<TR>(p, o, TR_STORE);
                     } else if (f32o && op.stats_out) {
                         // (sum, sumsq) of each row over this 128-feature tile: the 4
