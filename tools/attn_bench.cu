@@ -28,6 +28,17 @@ __device__ inline void tc_mma_ts_w(uint32_t d_tmem, uint32_t a_tmem, uint64_t bd
         "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+__device__ inline bool mbar_test_b(uint64_t* bar, uint32_t phase) {
+    uint32_t ok;
+    asm volatile("{ .reg .pred p; mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(ok) : "r"(smem_u32(bar)), "r"(phase) : "memory");
+    return ok != 0;
+}
+template <int MODE>
+__device__ inline void wait_sm(uint64_t* bar, uint32_t phase) {
+    if (MODE == 7) { while (!mbar_test_b(bar, phase)) {} }
+    else mbar_wait(bar, phase);
+}
 __device__ inline void tc_mma_w(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) { tc_mma_bf16_w(d, a, b, id, acc); }
 
 template <int MODE>  // 0: full pipeline; 1: no PV MMA (P published, no O); 2: softmax skips exps; 6: P in TMEM (TS MMA);
@@ -155,15 +166,19 @@ __global__ void __launch_bounds__(384, 1) k(int nblk, long long* out) {
         for (int j = 0; j < nblk; ++j) {
             if (j == 8) t0 = clock64();
             const int b = j & 1;
-            if (MODE >= 3) mbar_wait(&s_full4[j & 3], (j >> 2) & 1);
-            else mbar_wait(&s_full[b], (j >> 1) & 1);
+            const bool st = blockIdx.x == 0 && threadIdx.x == 128 && j >= 100 && j < 104;
+            long long* so = out + 2 + (j - 100) * 8;
+            if (st) so[0] = clock64();
+            if (MODE >= 3 && MODE <= 5) mbar_wait(&s_full4[j & 3], (j >> 2) & 1);
+            else wait_sm<MODE>(&s_full[b], (j >> 1) & 1);
+            if (st) so[1] = clock64();
             tc_fence_after();
             uint32_t sr[32];
-            tmem_ld32((MODE >= 3 ? tS4[j & 3] : tS[b]) + lane_off + hh * 32, sr);
+            tmem_ld32((MODE >= 3 && MODE <= 5 ? tS4[j & 3] : tS[b]) + lane_off + hh * 32, sr);
             tmem_ld_wait();
             tc_fence_before();
             __syncwarp();
-            if (lane == 0) mbar_arrive(MODE >= 3 ? &s_free4[j & 3] : &s_free[b]);
+            if (lane == 0) mbar_arrive(MODE >= 3 && MODE <= 5 ? &s_free4[j & 3] : &s_free[b]);
             const float* srf = reinterpret_cast<const float*>(sr);
             float t8[8];
 #pragma unroll
@@ -191,7 +206,9 @@ __global__ void __launch_bounds__(384, 1) k(int nblk, long long* out) {
                 pk[kk] = pack_bf16x2(p0, p1);
             }
             l = l * corr + (r4[0] + r4[1]) + (r4[2] + r4[3]);
-            if (j >= 2) mbar_wait(&p_free[b], ((j - 2) >> 1) & 1);
+            if (st) so[2] = clock64();
+            if (j >= 2) wait_sm<MODE>(&p_free[b], ((j - 2) >> 1) & 1);
+            if (st) so[3] = clock64();
             if (MODE == 6) {
                 tmem_st16(tP[b] + lane_off + hh * 16, pk);
                 tmem_st_wait();
@@ -222,6 +239,7 @@ __global__ void __launch_bounds__(384, 1) k(int nblk, long long* out) {
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&p_full[b]);
+            if (st) so[4] = clock64();
         }
         const long long t1 = clock64();
         if (blockIdx.x == 0 && threadIdx.x == 128) out[0] = (t1 - t0);
@@ -248,7 +266,19 @@ void run(long long* d, const char* name) {
 
 int main(int argc, char** argv) {
     long long* d;
-    cudaMalloc(&d, 16);
+    cudaMalloc(&d, 64 * 8);
+    if (argc > 1 && (atoi(argv[1]) == 9 || atoi(argv[1]) == 7)) {  // stamped run of the default pipeline
+        if (atoi(argv[1]) == 9) run<0>(d, "full pipeline (stamped)");
+        else run<7>(d, "softmax waits by test_wait polling");
+        long long h[64];
+        cudaMemcpy(h, d, sizeof(h), cudaMemcpyDeviceToHost);
+        for (int b = 0; b < 4; ++b) {
+            long long* so = h + 2 + b * 8;
+            printf("block %d: wait S %lld  S->exps done %lld  P slot wait %lld  P store+fence+arrive %lld  (total %lld)\n", b,
+                   so[1] - so[0], so[2] - so[1], so[3] - so[2], so[4] - so[3], so[4] - so[0]);
+        }
+        return 0;
+    }
     if (argc > 1) {  // one variant
         const int m = atoi(argv[1]);
         if (m == 6) run<6>(d, "P in TMEM (TS MMA for PV)");
