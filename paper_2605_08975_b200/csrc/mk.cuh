@@ -813,6 +813,7 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                                 waited = true;
                             }
                         }
+#pragma unroll 1
                         for (int i = 0; i < pre; ++i) {
                             const uint32_t st = (ks + i) % C::STAGES;
                             uint8_t* sb = slot_acquire(ks + i);
@@ -826,6 +827,7 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                             waited = true;
                         }
                         if (lane == 0) trace_ev<TR>(p, o, TR_DEP);
+#pragma unroll 1
                         for (int i = 0; i < g.nkb; ++i) {
                             const uint32_t st = (ks + i) % C::STAGES;
                             uint8_t* sb = smem + st * C::SLOT;
@@ -874,6 +876,7 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                             }
                         };
                         int pre = 0;
+#pragma unroll 1
                         while (pre < a.nj && pre < C::STAGES && a.g0 + pre < op.nbp) load_block(pre++);
                         if (p.flags & MK_ATT_L2PF) {
                             // the item's remaining prefix blocks (beyond the ring) into L2 now,
@@ -898,6 +901,7 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                         for (int pn = 0; pn < HD / 64; ++pn)
                             tma_load_2d_w(smem + C::OFF_Q + pn * C::QPANEL, op.tmQ, q_full,
                                         a.h * HD + pn * 64, a.row0);
+#pragma unroll 1
                         for (int j = pre; j < a.nj; ++j) load_block(j);
                         ks += a.nj;
                         ++natt;
@@ -922,6 +926,7 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                         const GemmItem g = gemm_item(op, it, op.tn);
                         if (nmma > 0) mbar_wait(acc_empty, (nmma - 1) & 1);
                         unsigned long long wsum = 0;
+#pragma unroll 1
                         for (int i = 0; i < g.nkb; ++i) {
                             const uint32_t st = (ks + i) % C::STAGES, ph = ((ks + i) / C::STAGES) & 1;
                             const long long w0 = TR ? clock64() : 0;
@@ -975,6 +980,7 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                             if (JJ - J < 6) if (lane == 0) trace_clk<TR>(p, o, TC_MPV + (JJ - J));
                         };
                         uint32_t prev_st = 0;
+#pragma unroll 1
                         for (int j = 0; j < a.nj; ++j) {
                             const uint32_t JJ = J + j;
                             const uint32_t st = (ks + j) % C::STAGES, ph = ((ks + j) / C::STAGES) & 1;
