@@ -840,7 +840,6 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                         }
                         ks += g.nkb;
                     }
-                    if (lane == 0 && !(p.flags & MK_NO_L2PF)) l2_share(op.pf_ptr, op.pf_bytes, wpol);
                 } else if (op.kind == OP_ATTN) {
                     if (lane == 0) tma_prefetch(op.tmW);
                     if (lane == 0) tma_prefetch(op.tmX);
@@ -906,8 +905,10 @@ __global__ void __launch_bounds__(384, 1) iter_kernel(const __grid_constant__ Pa
                         ks += a.nj;
                         ++natt;
                     }
-                    if (lane == 0 && !(p.flags & MK_NO_L2PF)) l2_share(op.pf_ptr, op.pf_bytes, wpol);
                 }
+                // one copy of the prefetch loop for both op kinds (code size)
+                if ((op.kind == OP_GEMM || op.kind == OP_ATTN) && lane == 0 && !(p.flags & MK_NO_L2PF))
+                    l2_share(op.pf_ptr, op.pf_bytes, wpol);
             }
         }
     } else if (warp == 1) {
